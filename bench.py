@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Bench: SSA firings/s of the bulk direct-method simulator on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step is one cwc_simulate call over the whole workload: every trajectory of
+the config simulated from t=0 to t_end with in-kernel sampling and the
+two-stage exact moment reduction (SURVEY §8(a) rows a1-a11 except the
+one-off model compile), inputs resident in HBM.  Default workload C2
+(BASELINE.json configs[1], the config its metric names): Lotka-Volterra,
+16384 replicas per GPU, t_end 10, 1001 samples, seed 1.  N GPUs: weak
+scaling -- each rank runs its own 16384-replica shard of one N*16384-replica
+run (distinct RNG streams) and the exact integer moments are merged with one
+all-reduce per step.
+
+`--impl reference` times the CPU oracle (oracle/, single-threaded, as it
+stands) on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as wl  # noqa: E402
+
+METRIC = "SSA firings/sec on 1 B200 (replicas×firings); % of issue roofline"
+
+# Algorithmic thread-level operations of one direct-method firing
+# (SURVEY §8(d) "Algorithmic work per firing").
+PHILOX_OPS = 60      # 10 rounds x (2 mul-hi/lo, 2 xor3, 2 key adds)
+UNIFORM_OPS = 6      # two 53-bit conversions
+LOG_OPS = 30         # fp64 log fast path
+DIV_OPS = 10         # fp64 division (rcp + Newton + fix-up)
+LOOP_OPS = 4         # t += tau, crossing compare, counters
+
+
+def alg_ops_per_firing(M, avg_nu, avg_dep=None):
+    """Thread path: full recompute (4 ops per propensity), M-1 adds, M
+    compares; warp path: |D(mu)| recomputes, M-1 adds, M/2 compares."""
+    base = PHILOX_OPS + UNIFORM_OPS + LOG_OPS + DIV_OPS + LOOP_OPS + 2 * avg_nu
+    if avg_dep is None:
+        return base + 4 * M + (M - 1) + M
+    return base + 4 * avg_dep + (M - 1) + M / 2
+
+
+def _rank_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.path = os.path.join("/tmp", "cwc_clocks_%d_%d.csv" % (os.getpid(), device_index))
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.dev)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_sample(desc, sweep, cfg, g_list):
+    """Time the oracle (single thread, as it stands) on trajectories g_list."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    r = oracle.simulate(desc, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep,
+                        g_list=g_list, want_traj=False, want_stats=True)
+    dt = time.perf_counter() - t0
+    return int(r["firings"].sum()), dt
+
+
+def _sample_size(name):
+    # trajectories per ~10-15 s of single-core oracle work (BASELINE.md §4 rates)
+    return {"C1": 1024, "C2": 384, "C3": 2048, "C4": 192, "C5": 12}[name]
+
+
+def run_reference(args):
+    rank, world, _ = _rank_env()
+    if rank != 0:
+        return 0
+    desc, sweep, cfg = wl.config(args.config)
+    G = (len(sweep["values"]) if sweep else 1) * cfg["n_replicas"]
+    per_step = max(1, _sample_size(args.config) // 6)
+    stride = max(1, G // (per_step * (args.steps + args.warmup) + 1))
+    steps = []
+    for k in range(args.warmup + args.steps):
+        g = [(k * per_step + i) * stride % G for i in range(per_step)]
+        f, dt = oracle_sample(desc, sweep, cfg, g)
+        if k >= args.warmup:
+            steps.append((f, dt))
+    F = sum(s[0] for s in steps)
+    T = sum(s[1] for s in steps)
+    value = F / T
+    sample = "%d trajectories per step (stride %d over g) of %s, full t_end" % (per_step, stride, args.config)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "firings/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_block(args.config, cfg, sweep, args.gpus, "cpu-oracle"),
+            "cpu_baseline": {"value": value, "unit": "firings/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": _cpu_model()},
+            "e2e": {"value": value, "unit": "firings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_block(name, cfg, sweep, n_gpus, path):
+    P = len(sweep["values"]) if sweep else 1
+    return {"workload": "%s %s" % (name, wl.CONFIGS[name]["desc"]), "points": P,
+            "replicas_per_point_per_gpu": cfg["n_replicas"], "t_end": cfg["t_end"], "sample_dt": cfg["sample_dt"],
+            "samples": int(np.floor(cfg["t_end"] / cfg["sample_dt"])) + 1, "seed": cfg["seed"], "path": path,
+            "parallelism": "dp%d (replica shards; exact int64 moment all-reduce)" % n_gpus,
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1010_2438_b200 import cwc
+    from paper_1010_2438_b200.dist import allreduce_stats
+
+    rank, world, local = _rank_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    desc, sweep, cfg = wl.config(args.config)
+    model = cwc.cwc_model_create(desc)
+    flat = model.get_flat()
+    info = model.info
+    M = info.n_reactions
+    avg_nu = float(np.mean(np.diff(flat["nu_ptr"]))) if M else 0.0
+    avg_dep = float(np.mean(np.diff(flat["dep_ptr"]))) if M else 0.0
+    path = "warp" if info.path == cwc.CWC_PATH_WARP else "thread"
+
+    R = cfg["n_replicas"]
+    P = len(sweep["values"]) if sweep else 1
+    J1 = int(np.floor(cfg["t_end"] / cfg["sample_dt"])) + 1
+    O = info.n_obs
+    ncell = P * J1 * O
+    G = P * R
+
+    count = torch.empty(ncell, dtype=torch.int64, device=dev)
+    s1 = torch.empty(ncell, dtype=torch.int64, device=dev)
+    sq = torch.empty((ncell, 2), dtype=torch.int64, device=dev)
+    firings = torch.empty(G, dtype=torch.int64, device=dev)
+    status = torch.empty(G, dtype=torch.int32, device=dev)
+    ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_k0.record(stream)
+    ev_k1.record(stream)
+    opts = cwc.cwc_sim_opts()
+    opts.force_path = cwc.CWC_PATH_AUTO
+    opts.out_firings = firings.data_ptr()
+    opts.out_status = status.data_ptr()
+    opts.replica_offset = rank * R
+    opts.replicas_total = world * R
+    opts.ev_kernel_begin = ev_k0.cuda_event
+    opts.ev_kernel_end = ev_k1.cuda_event
+    ws_bytes = cwc.cwc_simulate_workspace_size(model, R, sweep, cfg["t_end"], cfg["sample_dt"], opts)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        cwc.cwc_simulate(model, R, sweep, cfg["t_end"], cfg["sample_dt"], cfg["seed"], stream.cuda_stream,
+                         (count, s1, sq), ws, opts)
+        allreduce_stats(count, s1, sq)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    fired = int(firings.sum().item())          # identical every step (same seed, same shard)
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kms = []
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    clocks = ClockSampler(vis.split(",")[local] if vis else local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        ev0[k].record(stream)
+        step()
+        ev1[k].record(stream)
+        ev1[k].synchronize()
+        kms.append(ev_k0.elapsed_time(ev_k1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    f = torch.tensor([fired], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f, op=dist.ReduceOp.SUM)
+    total_ms = float(t.item())
+    fired_all = int(f.item())
+    value = fired_all * args.steps / (total_ms / 1e3)
+
+    # end-to-end through the public API with host buffers (H2D + D2H in the timed region)
+    hc = torch.empty(ncell, dtype=torch.int64, pin_memory=True)
+    hs = torch.empty(ncell, dtype=torch.int64, pin_memory=True)
+    hq = torch.empty((ncell, 2), dtype=torch.int64, pin_memory=True)
+    hws_bytes = cwc.cwc_simulate_host_workspace_size(model, R, sweep, cfg["t_end"], cfg["sample_dt"])
+    hws = torch.empty(hws_bytes, dtype=torch.uint8, device=dev)
+    sw_arrays = cwc._SweepArrays(sweep) if sweep is not None else None
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        a.record(stream)
+        cwc.cwc_simulate_host(model, R, sweep, cfg["t_end"], cfg["sample_dt"], cfg["seed"], stream.cuda_stream,
+                              (hc, hs, hq), hws, sweep_arrays=sw_arrays)
+        b.record(stream)
+        b.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e_total = sum(e2e_ms)
+    te = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = fired_all * args.steps / (float(te.item()) / 1e3)
+
+    # roofline of the dominant kernel (the SSA kernel), instruction issue bound
+    props = torch.cuda.get_device_properties(dev)
+    peaks = _peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_ops = props.multi_processor_count * 4 * 32 * f_max
+    ops = alg_ops_per_firing(M, avg_nu, avg_dep if path == "warp" else None)
+    k_ms = float(np.mean(kms))
+    achieved = ops * fired / (k_ms / 1e3)
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
+                "frac": achieved / peak_ops, "traffic": None,
+                "ops_per_firing": ops, "kernel": "ssa_%s_kernel" % path, "kernel_ms": k_ms,
+                "peak_source": "issue peak = %d SMs x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
+                % (props.multi_processor_count, f_max / 1e6)}
+
+    line = {"metric": METRIC, "value": value, "unit": "firings/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_block(args.config, cfg, sweep, world, path),
+            "firings_per_step": fired_all, "kernel_ms_per_step": k_ms,
+            "roofline": roofline,
+            "e2e": {"value": e2e_value, "unit": "firings/s", "h2d_bytes_per_step": 8 * P * max(M, 1),
+                    "d2h_bytes_per_step": 32 * ncell},
+            "gpu_launches": 2 * args.steps, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n = _sample_size(args.config)
+        g_list = list(range(0, G, max(1, G // n)))[:n]
+        fo, dto = oracle_sample(desc, sweep, cfg, g_list)
+        line["cpu_baseline"] = {"value": fo / dto, "unit": "firings/s", "cores": 1, "kind": "oracle",
+                                "sample": "%d of %d trajectories of %s (every %d-th g), full t_end; %.1f s"
+                                % (len(g_list), G, args.config, max(1, G // n), dto),
+                                "cpu": _cpu_model()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

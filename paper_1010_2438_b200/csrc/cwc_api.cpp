@@ -1,0 +1,684 @@
+// cwc_api.cpp -- the C ABI (include/cwc.h): model compiler and launcher.
+//
+// cwc_model_create validates the CWC description and flattens its rules over
+// the fixed compartment tree (rule-major, context in index order = preorder,
+// then child in index order), merges each pattern into
+// (cell, multiplicity) reactants (a pattern is a multiset), forms
+// the net change nu = products - reactants and the dependency
+// graph D(mu) = {m : reactants(m) meet changed(mu)}, and uploads the tables.
+// cwc_simulate carves the caller's workspace, picks the kernel and launch
+// shape, and enqueues SSA kernel + stage-2 reduction on the caller's stream.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <algorithm>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "cwc.h"
+#include "cwc_internal.h"
+
+using namespace cwc;
+
+namespace {
+
+thread_local std::string g_err;
+
+cwc_status fail(cwc_status s, const std::string &msg) {
+    g_err = msg;
+    return s;
+}
+cwc_status cuda_fail(cudaError_t e, const char *where) {
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return CWC_ERR_CUDA;
+}
+
+struct DeviceBuf {
+    void *p = nullptr;
+    ~DeviceBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+}  // namespace
+
+struct cwc_model_s {
+    // host copies
+    int32_t n_species = 0, n_compartments = 0, n_cells = 0, M = 0, n_obs = 0, n_rules = 0;
+    std::vector<double> rule_rate;
+    std::vector<int32_t> entry_rule, entry_ctx, entry_child;
+    std::vector<int32_t> re_ptr, re_cell, re_mult;
+    std::vector<int32_t> nu_ptr, nu_cell, nu_delta;
+    std::vector<int32_t> dep_ptr, dep;
+    std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
+    std::vector<ReactionDesc> rx;
+    int max_deps = 0;
+    bool thread_ok = false;
+    ThreadTables tt{};
+    // device copies (one allocation)
+    DeviceBuf dev;
+    WarpTables wt{};
+    int device = 0;
+};
+
+namespace {
+
+bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+
+cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
+    if (!d) return fail(CWC_ERR_INVALID, "desc is NULL");
+    const int S = d->n_species, C = d->n_compartments, NT = d->n_types;
+    if (S < 1) return fail(CWC_ERR_INVALID, "n_species must be >= 1");
+    if (C < 1) return fail(CWC_ERR_INVALID, "n_compartments must be >= 1");
+    if (NT < 1) return fail(CWC_ERR_INVALID, "n_types must be >= 1");
+    if ((long long)S * C > (1ll << 30)) return fail(CWC_ERR_INVALID, "too many cells");
+    if (!d->parent || !d->type) return fail(CWC_ERR_INVALID, "parent/type are NULL");
+    if (d->parent[0] != -1 || d->type[0] != 0) return fail(CWC_ERR_INVALID, "compartment 0 must be the root of type 0");
+    for (int c = 0; c < C; ++c) {
+        if (d->type[c] < 0 || d->type[c] >= NT) return fail(CWC_ERR_INVALID, "type out of range at compartment " + std::to_string(c));
+        if (c > 0 && (d->parent[c] < 0 || d->parent[c] >= c))
+            return fail(CWC_ERR_INVALID, "parent must satisfy 0 <= parent[c] < c (preorder) at compartment " + std::to_string(c));
+    }
+    const int R = d->n_rules;
+    if (R < 0) return fail(CWC_ERR_INVALID, "n_rules < 0");
+    if (R > 0 && (!d->rule_label || !d->rule_child_label || !d->re_ptr || !d->pr_ptr || !d->rate))
+        return fail(CWC_ERR_INVALID, "rule arrays are NULL");
+    const int ncell = S * C;
+    if (!d->init) return fail(CWC_ERR_INVALID, "init is NULL");
+    for (int i = 0; i < ncell; ++i)
+        if (d->init[i] < 0) return fail(CWC_ERR_INVALID, "negative initial count at cell " + std::to_string(i));
+    if (d->n_obs < 0) return fail(CWC_ERR_INVALID, "n_obs < 0");
+    if (d->n_obs > 0 && !d->obs_of_cell) return fail(CWC_ERR_INVALID, "obs_of_cell is NULL");
+    for (int i = 0; d->n_obs > 0 && i < ncell; ++i)
+        if (d->obs_of_cell[i] < -1 || d->obs_of_cell[i] >= d->n_obs)
+            return fail(CWC_ERR_INVALID, "obs_of_cell out of range at cell " + std::to_string(i));
+
+    m->n_species = S;
+    m->n_compartments = C;
+    m->n_cells = ncell;
+    m->n_rules = R;
+    m->n_obs = d->n_obs;
+    m->rule_rate.assign(d->rate, d->rate + R);
+    for (int r = 0; r < R; ++r) {
+        if (!finite_pos(d->rate[r])) return fail(CWC_ERR_INVALID, "rate must be finite and > 0 (rule " + std::to_string(r) + ")");
+        if (d->rule_label[r] < 0 || d->rule_label[r] >= NT) return fail(CWC_ERR_INVALID, "rule_label out of range (rule " + std::to_string(r) + ")");
+        if (d->rule_child_label[r] < -1 || d->rule_child_label[r] >= NT)
+            return fail(CWC_ERR_INVALID, "rule_child_label out of range (rule " + std::to_string(r) + ")");
+        for (int side = 0; side < 2; ++side) {
+            const int32_t *ptr = side ? d->pr_ptr : d->re_ptr;
+            const int32_t *wh = side ? d->pr_where : d->re_where;
+            const int32_t *sp = side ? d->pr_species : d->re_species;
+            const int32_t *mu = side ? d->pr_mult : d->re_mult;
+            if (ptr[r] < 0 || ptr[r + 1] < ptr[r]) return fail(CWC_ERR_INVALID, "bad CSR pointer (rule " + std::to_string(r) + ")");
+            int order = 0;
+            for (int q = ptr[r]; q < ptr[r + 1]; ++q) {
+                if (!wh || !sp || !mu) return fail(CWC_ERR_INVALID, "pattern arrays are NULL");
+                if (wh[q] != 0 && wh[q] != 1) return fail(CWC_ERR_INVALID, "where must be 0 or 1 (rule " + std::to_string(r) + ")");
+                if (wh[q] == 1 && d->rule_child_label[r] < 0)
+                    return fail(CWC_ERR_INVALID, "child-compartment species on a local rule (rule " + std::to_string(r) + ")");
+                if (sp[q] < 0 || sp[q] >= S) return fail(CWC_ERR_INVALID, "species out of range (rule " + std::to_string(r) + ")");
+                if (mu[q] < 1) return fail(CWC_ERR_INVALID, "mult must be >= 1 (rule " + std::to_string(r) + ")");
+                order += mu[q];
+            }
+            if (side == 0 && order > 2)
+                return fail(CWC_ERR_UNSUPPORTED, "reaction order > 2 is not supported (rule " + std::to_string(r) + ")");
+        }
+    }
+
+    // children lists in index order
+    std::vector<std::vector<int>> kids(C);
+    for (int c = 1; c < C; ++c) kids[d->parent[c]].push_back(c);
+
+    m->re_ptr.push_back(0);
+    m->nu_ptr.push_back(0);
+    for (int r = 0; r < R; ++r) {
+        const int lab = d->rule_label[r], cl = d->rule_child_label[r];
+        for (int c = 0; c < C; ++c) {
+            if (d->type[c] != lab) continue;
+            std::vector<int> childs;
+            if (cl < 0) childs.push_back(-1);
+            else
+                for (int k : kids[c])
+                    if (d->type[k] == cl) childs.push_back(k);
+            for (int ch : childs) {
+                std::map<int, int> re, pr;
+                for (int q = d->re_ptr[r]; q < d->re_ptr[r + 1]; ++q)
+                    re[(d->re_where[q] ? ch : c) * S + d->re_species[q]] += d->re_mult[q];
+                for (int q = d->pr_ptr[r]; q < d->pr_ptr[r + 1]; ++q)
+                    pr[(d->pr_where[q] ? ch : c) * S + d->pr_species[q]] += d->pr_mult[q];
+                m->entry_rule.push_back(r);
+                m->entry_ctx.push_back(c);
+                m->entry_child.push_back(ch);
+                ReactionDesc rd{ncell, ncell, 0, r};
+                int slot = 0;
+                for (auto &kv : re) {
+                    m->re_cell.push_back(kv.first);
+                    m->re_mult.push_back(kv.second);
+                    if (kv.second == 2) {
+                        rd.ia = rd.ib = kv.first;
+                        rd.kind = 1 | (1 << 1);
+                    } else if (slot == 0) {
+                        rd.ia = kv.first;
+                    } else {
+                        rd.ib = kv.first;
+                    }
+                    ++slot;
+                }
+                m->re_ptr.push_back((int32_t)m->re_cell.size());
+                std::map<int, int> nu;
+                for (auto &kv : pr) nu[kv.first] += kv.second;
+                for (auto &kv : re) nu[kv.first] -= kv.second;
+                for (auto &kv : nu)
+                    if (kv.second != 0) {
+                        m->nu_cell.push_back(kv.first);
+                        m->nu_delta.push_back(kv.second);
+                    }
+                m->nu_ptr.push_back((int32_t)m->nu_cell.size());
+                m->rx.push_back(rd);
+            }
+        }
+    }
+    m->M = (int32_t)m->entry_rule.size();
+    const int M = m->M;
+
+    // dependency graph: reactions reading each cell, then union per mu
+    std::vector<std::vector<int>> readers(ncell);
+    for (int k = 0; k < M; ++k)
+        for (int q = m->re_ptr[k]; q < m->re_ptr[k + 1]; ++q) readers[m->re_cell[q]].push_back(k);
+    m->dep_ptr.push_back(0);
+    std::vector<int> mark(M, -1);
+    for (int mu = 0; mu < M; ++mu) {
+        std::vector<int> row;
+        for (int q = m->nu_ptr[mu]; q < m->nu_ptr[mu + 1]; ++q)
+            for (int k : readers[m->nu_cell[q]])
+                if (mark[k] != mu) {
+                    mark[k] = mu;
+                    row.push_back(k);
+                }
+        std::sort(row.begin(), row.end());
+        m->dep.insert(m->dep.end(), row.begin(), row.end());
+        m->dep_ptr.push_back((int32_t)m->dep.size());
+        if ((int)row.size() > m->max_deps) m->max_deps = (int)row.size();
+    }
+
+    m->init.assign(d->init, d->init + ncell);
+    if (m->n_obs > 0) m->obs_of_cell.assign(d->obs_of_cell, d->obs_of_cell + ncell);
+    else m->obs_of_cell.assign(ncell, -1);
+    m->obs_ptr.assign(m->n_obs + 1, 0);
+    for (int o = 0; o < m->n_obs; ++o) {
+        for (int c = 0; c < ncell; ++c)
+            if (m->obs_of_cell[c] == o) m->obs_cells.push_back(c);
+        m->obs_ptr[o + 1] = (int32_t)m->obs_cells.size();
+    }
+
+    // thread path tables
+    bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
+    for (size_t q = 0; ok && q < m->nu_delta.size(); ++q)
+        if (m->nu_delta[q] < -127 || m->nu_delta[q] > 127) ok = false;
+    m->thread_ok = ok;
+    if (ok) {
+        ThreadTables &tt = m->tt;
+        std::memset(&tt, 0, sizeof(tt));
+        tt.n_cells = ncell;
+        tt.M = M;
+        tt.O = m->n_obs;
+        for (int k = 0; k < kThreadMaxReactions; ++k) {
+            tt.ia[k] = tt.ib[k] = -1;  // -1 reads the constant 1
+            tt.sub[k] = tt.shr[k] = 0;
+            tt.nu_pack[k] = 0;
+        }
+        for (int k = 0; k < M; ++k) {
+            tt.ia[k] = m->rx[k].ia == ncell ? -1 : m->rx[k].ia;
+            tt.ib[k] = m->rx[k].ib == ncell ? -1 : m->rx[k].ib;
+            tt.sub[k] = m->rx[k].kind & 1;
+            tt.shr[k] = m->rx[k].kind >> 1;
+            uint64_t pack = 0;
+            for (int q = m->nu_ptr[k]; q < m->nu_ptr[k + 1]; ++q)
+                pack |= (uint64_t)(uint8_t)(int8_t)m->nu_delta[q] << (8 * m->nu_cell[q]);
+            tt.nu_pack[k] = pack;
+        }
+        for (int c = 0; c < kThreadMaxCells; ++c) {
+            tt.obs_of[c] = c < ncell ? m->obs_of_cell[c] : -1;
+            tt.init[c] = c < ncell ? m->init[c] : 0;
+        }
+    }
+    return CWC_OK;
+}
+
+template <typename T>
+size_t push_bytes(std::vector<unsigned char> &blob, const std::vector<T> &v) {
+    size_t off = (blob.size() + 255) & ~size_t(255);
+    blob.resize(off + std::max<size_t>(v.size() * sizeof(T), 16));
+    if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+}
+
+cwc_status upload(cwc_model_s *m) {
+    int ndev = 0;
+    cudaError_t e0 = cudaGetDeviceCount(&ndev);
+    if (e0 != cudaSuccess || ndev == 0) return fail(CWC_ERR_CUDA, "no CUDA device (there is no CPU fallback)");
+    std::vector<unsigned char> blob;
+    std::vector<int2> nu2(m->nu_cell.size());
+    for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
+    const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
+                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep), o_op = push_bytes(blob, m->obs_ptr),
+                 o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
+    cudaError_t e = cudaGetDevice(&m->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaGetDevice");
+    e = cudaMalloc(&m->dev.p, blob.size());
+    if (e == cudaErrorMemoryAllocation) return fail(CWC_ERR_NOMEM, "cwc_model_create: device tables");
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaMalloc");
+    e = cudaMemcpy(m->dev.p, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaMemcpy");
+    unsigned char *b = (unsigned char *)m->dev.p;
+    WarpTables &w = m->wt;
+    w.n_cells = m->n_cells;
+    w.M = m->M;
+    w.O = m->n_obs;
+    w.B = std::max(1, (m->M + 31) / 32);
+    w.rx = (const ReactionDesc *)(b + o_rx);
+    w.nu_ptr = (const int32_t *)(b + o_nup);
+    w.nu = (const int2 *)(b + o_nu);
+    w.dep_ptr = (const int32_t *)(b + o_dp);
+    w.dep = (const int32_t *)(b + o_dep);
+    w.obs_ptr = (const int32_t *)(b + o_op);
+    w.obs_cells = (const int32_t *)(b + o_oc);
+    w.init = (const int32_t *)(b + o_init);
+    return CWC_OK;
+}
+
+// ---- launch planning ----------------------------------------------------------
+struct Plan {
+    int path = 0;
+    int64_t G = 0, R = 0;
+    int32_t P = 1, J = 0;
+    int64_t n_stat_cells = 0;  // P * (J+1) * O
+    // thread path
+    int threads = 128;
+    int s_pad = 0, m_pad = 0;
+    // warp path
+    int warps_per_block = 4;
+    int blocks = 0;
+    // stats
+    int stats_smem = 0;
+    int64_t cells_per_part = 0;
+    int n_parts = 1;
+    int64_t traj_per_part = 0;
+    size_t smem_bytes = 0;
+    // workspace layout
+    size_t off_rates = 0, off_parts = 0, off_trace = 0, off_counter = 0, off_stats = 0, total = 0;
+};
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+const char *env(const char *k) {
+    const char *v = std::getenv(k);
+    return (v && *v) ? v : nullptr;
+}
+
+int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt,
+                    const cwc_sim_opts *opts, bool host_stats, Plan &pl) {
+    if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
+    if (!(t_end > 0.0) || !std::isfinite(t_end)) return fail(CWC_ERR_INVALID, "t_end must be finite and > 0");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(CWC_ERR_INVALID, "sample_dt must be finite and > 0");
+    if (dt > t_end) return fail(CWC_ERR_INVALID, "sample_dt must be <= t_end");
+    if (n_replicas < 1) return fail(CWC_ERR_INVALID, "n_replicas must be >= 1");
+    const double Jd = std::floor(t_end / dt);
+    if (Jd > 2e9) return fail(CWC_ERR_INVALID, "too many samples");
+    pl.J = (int32_t)Jd;
+    pl.P = 1;
+    if (sweep) {
+        if (sweep->n_points < 1) return fail(CWC_ERR_INVALID, "sweep.n_points must be >= 1");
+        if (sweep->n_swept < 0 || (sweep->n_swept > 0 && (!sweep->rule || !sweep->value)))
+            return fail(CWC_ERR_INVALID, "bad sweep arrays");
+        for (int i = 0; i < sweep->n_swept; ++i)
+            if (sweep->rule[i] < 0 || sweep->rule[i] >= m->n_rules) return fail(CWC_ERR_INVALID, "sweep rule id out of range");
+        for (long long i = 0; i < (long long)sweep->n_points * sweep->n_swept; ++i)
+            if (!finite_pos(sweep->value[i])) return fail(CWC_ERR_INVALID, "sweep value must be finite and > 0");
+        pl.P = sweep->n_points;
+    }
+    pl.R = n_replicas;
+    if ((double)pl.P * (double)n_replicas > 9e18 / 2) return fail(CWC_ERR_INVALID, "too many trajectories");
+    pl.G = (int64_t)pl.P * n_replicas;
+    const int64_t J1 = (int64_t)pl.J + 1;
+    const int O = m->n_obs;
+    pl.n_stat_cells = (int64_t)pl.P * J1 * O;
+    const int nsm = sm_count();
+
+    int force = opts ? opts->force_path : CWC_PATH_AUTO;
+    if (const char *e = env("CWC_FORCE_PATH")) force = std::atoi(e);
+    if (force == CWC_PATH_THREAD && !m->thread_ok) return fail(CWC_ERR_INVALID, "thread path cannot run this model (too many cells/reactions/observables)");
+    pl.path = (force == CWC_PATH_AUTO) ? (m->thread_ok ? CWC_PATH_THREAD : CWC_PATH_WARP) : force;
+    if (pl.path != CWC_PATH_THREAD && pl.path != CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "bad force_path");
+    int bt = opts ? opts->block_threads : 0;
+    if (const char *e = env("CWC_BLOCK_THREADS")) bt = std::atoi(e);
+    if (bt != 0 && (bt < 32 || bt > 256 || bt % 32)) return fail(CWC_ERR_INVALID, "block_threads must be a multiple of 32 in [32, 256]");
+    const char *smode = env("CWC_STATS_MODE");
+    const size_t smem_cap = 200 * 1024;
+
+    if (pl.path == CWC_PATH_THREAD) {
+        pl.s_pad = thread_pad_cells(m->n_cells);
+        pl.m_pad = thread_pad_reactions(std::max(m->M, 2));
+        if (pl.s_pad < 0 || pl.m_pad < 0) return fail(CWC_ERR_INVALID, "thread path padding");
+        int T = bt;
+        if (!T) {
+            T = 32;
+            for (int cand : {64, 128, 256})
+                if ((pl.G + cand - 1) / cand >= 2ll * nsm) T = cand;
+        }
+        pl.threads = T;
+        const int64_t blocks = (pl.G + T - 1) / T;
+        if (blocks > 0x7fffffffll) return fail(CWC_ERR_INVALID, "too many trajectories for one launch");
+        pl.blocks = (int)blocks;
+        // points touched by one block
+        int64_t np_max = 1;
+        for (int64_t b = 0; b < blocks; ++b) {
+            const int64_t pf = (b * T) / pl.R, plst = (std::min<int64_t>((b + 1) * T, pl.G) - 1) / pl.R;
+            np_max = std::max(np_max, plst - pf + 1);
+            if (np_max >= pl.P) break;
+        }
+        const int64_t cells = ((np_max * J1 * O) + 1) & ~int64_t(1);
+        const size_t smem = (size_t)(24 * cells);
+        const int64_t resident_needed = (blocks + nsm - 1) / nsm;
+        bool use_smem = smem <= smem_cap && (int64_t)smem * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
+        if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
+        if (O == 0) use_smem = false;
+        if (use_smem) {
+            pl.stats_smem = 1;
+            pl.cells_per_part = std::max<int64_t>(cells, 2);
+            pl.n_parts = pl.blocks;
+            pl.traj_per_part = T;
+            pl.smem_bytes = smem;
+        } else {
+            pl.stats_smem = 0;
+            pl.cells_per_part = std::max<int64_t>((pl.n_stat_cells + 1) & ~int64_t(1), 2);
+            const int64_t budget = (int64_t)256 << 20;
+            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / (24 * pl.cells_per_part)));
+            pl.n_parts = (int)np;
+            pl.traj_per_part = 0;
+            pl.smem_bytes = 0;
+        }
+    } else {
+        const WarpTables &w = m->wt;
+        int W = bt ? bt / 32 : 4;
+        if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
+        pl.warps_per_block = W;
+        const size_t per_warp = warp_smem_per_warp(w);
+        const int64_t cells = std::max<int64_t>((pl.n_stat_cells + 1) & ~int64_t(1), 2);
+        const size_t stats = (size_t)(24 * cells);
+        bool use_smem = stats + W * per_warp <= 96 * 1024;
+        if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
+        if (O == 0) use_smem = false;
+        pl.stats_smem = use_smem ? 1 : 0;
+        pl.cells_per_part = cells;
+        pl.smem_bytes = (use_smem ? stats : 0) + W * per_warp;
+        if (pl.smem_bytes > smem_cap + 27 * 1024) return fail(CWC_ERR_UNSUPPORTED, "warp path: per-warp state does not fit in shared memory");
+        // persistent grid: resident blocks on all SMs
+        int per_sm = 1;
+        // occupancy by shared memory / threads
+        const int by_smem = (int)std::max<size_t>(1, (228 * 1024) / (pl.smem_bytes + 1024));
+        const int by_threads = std::max(1, 2048 / (W * 32));
+        per_sm = std::min(by_smem, by_threads);
+        if (const char *e = env("CWC_BLOCKS_PER_SM")) per_sm = std::atoi(e);
+        int64_t blocks = (int64_t)nsm * per_sm;
+        blocks = std::min<int64_t>(blocks, (pl.G + W - 1) / W);
+        pl.blocks = (int)std::max<int64_t>(1, blocks);
+        pl.threads = W * 32;
+        pl.traj_per_part = 0;
+        if (use_smem) {
+            pl.n_parts = pl.blocks;
+        } else {
+            const int64_t budget = (int64_t)512 << 20;
+            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / (24 * cells)));
+        }
+    }
+
+    // workspace
+    size_t off = 0;
+    pl.off_rates = off;
+    off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
+    pl.off_parts = off;
+    off = align256(off + (size_t)24 * pl.cells_per_part * pl.n_parts);
+    pl.off_trace = off;
+    off = align256(off + sizeof(int64_t) * (size_t)std::max(opts ? opts->n_trace : 0, 1));
+    pl.off_counter = off;
+    off = align256(off + 16);
+    pl.off_stats = off;
+    if (host_stats) off = align256(off + (size_t)32 * std::max<int64_t>(pl.n_stat_cells, 1));
+    pl.total = off;
+    return CWC_OK;
+}
+
+cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt, uint64_t seed,
+               void *stream_, cwc_stats st, void *ws, size_t ws_bytes, const cwc_sim_opts *opts, bool host_stats,
+               cwc_stats host_out) {
+    if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
+    if (!m->dev.p) {  // tables go to the device on first use (host-only creation needs no GPU)
+        cwc_status su = upload(m);
+        if (su != CWC_OK) return su;
+    }
+    Plan pl;
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, dt, opts, host_stats, pl);
+    if (s != CWC_OK) return s;
+    if (!ws && pl.total > 0) return fail(CWC_ERR_INVALID, "workspace is NULL");
+    if (ws_bytes < pl.total) return fail(CWC_ERR_INVALID, "workspace too small: need " + std::to_string(pl.total) + " bytes");
+    if (opts && opts->n_trace > 0 && (!opts->trace_g || !opts->trace_buf || !opts->trace_len || opts->trace_cap < 1))
+        return fail(CWC_ERR_INVALID, "trace arguments incomplete");
+    if (pl.n_stat_cells > 0 && (!st.count || !st.sum || !st.sumsq)) return fail(CWC_ERR_INVALID, "stats pointers are NULL");
+    cudaStream_t stream = (cudaStream_t)stream_;
+    unsigned char *w = (unsigned char *)ws;
+
+    // per-point flat rates [P][M] (host expansion of the sweep)
+    const int M = m->M;
+    std::vector<double> rates((size_t)pl.P * std::max(M, 1), 0.0);
+    std::vector<double> rule_rates(m->rule_rate);
+    for (int p = 0; p < pl.P; ++p) {
+        if (sweep)
+            for (int i = 0; i < sweep->n_swept; ++i) rule_rates[sweep->rule[i]] = sweep->value[(size_t)p * sweep->n_swept + i];
+        for (int k = 0; k < M; ++k) rates[(size_t)p * M + k] = rule_rates[m->entry_rule[k]];
+    }
+    cudaError_t e = cudaMemcpyAsync(w + pl.off_rates, rates.data(), sizeof(double) * rates.size(), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: rates upload");
+
+    RunParams rp{};
+    rp.G = pl.G;
+    rp.R = pl.R;
+    rp.R_total = pl.R;
+    rp.r_off = 0;
+    rp.P = pl.P;
+    rp.J = pl.J;
+    rp.dt = dt;
+    rp.seed = seed;
+    rp.rates = (const double *)(w + pl.off_rates);
+    rp.parts = w + pl.off_parts;
+    rp.cells_per_part = pl.cells_per_part;
+    rp.stats_smem = pl.stats_smem;
+    rp.n_parts = pl.n_parts;
+    rp.traj_per_part = pl.traj_per_part;
+    rp.next_traj = (unsigned long long *)(w + pl.off_counter);
+    if (opts) {
+        if (opts->replicas_total != 0) {
+            if (opts->replica_offset < 0 || opts->replicas_total < opts->replica_offset + n_replicas)
+                return fail(CWC_ERR_INVALID, "replica_offset + n_replicas must be <= replicas_total");
+            rp.R_total = opts->replicas_total;
+            rp.r_off = opts->replica_offset;
+        } else if (opts->replica_offset != 0) {
+            return fail(CWC_ERR_INVALID, "replica_offset needs replicas_total");
+        }
+        rp.out_traj = opts->out_traj;
+        rp.out_firings = opts->out_firings;
+        rp.out_status = opts->out_status;
+        if (opts->n_trace > 0) {
+            e = cudaMemcpyAsync(w + pl.off_trace, opts->trace_g, sizeof(int64_t) * opts->n_trace, cudaMemcpyHostToDevice, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: trace ids upload");
+            e = cudaMemsetAsync(opts->trace_len, 0, sizeof(int64_t) * opts->n_trace, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: trace_len");
+            rp.trace_g = (const int64_t *)(w + pl.off_trace);
+            rp.n_trace = opts->n_trace;
+            rp.trace_cap = opts->trace_cap;
+            rp.trace_buf = opts->trace_buf;
+            rp.trace_len = opts->trace_len;
+        }
+    }
+    if (!pl.stats_smem) {
+        e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)24 * pl.cells_per_part * pl.n_parts, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: zero partials");
+    }
+    e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: counter");
+
+    cudaEvent_t ev0 = opts ? (cudaEvent_t)opts->ev_kernel_begin : nullptr;
+    cudaEvent_t ev1 = opts ? (cudaEvent_t)opts->ev_kernel_end : nullptr;
+    if (ev0 && (e = cudaEventRecord(ev0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_begin");
+    if (pl.path == CWC_PATH_THREAD) {
+        e = launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_thread launch");
+    } else {
+        e = launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_warp launch");
+    }
+    if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_end");
+    cwc_stats dst = st;
+    if (host_stats) {
+        unsigned char *sb = w + pl.off_stats;
+        dst.count = (int64_t *)sb;
+        dst.sum = (int64_t *)(sb + 8 * pl.n_stat_cells);
+        dst.sumsq = (uint64_t *)(sb + 16 * pl.n_stat_cells);
+    }
+    if (pl.n_stat_cells > 0) {
+        e = launch_stats_stage2(rp, m->n_obs, dst.count, dst.sum, dst.sumsq, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: stage-2 launch");
+        if (host_stats) {
+            const size_t n8 = 8 * (size_t)pl.n_stat_cells;
+            if ((e = cudaMemcpyAsync(host_out.count, dst.count, n8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(host_out.sum, dst.sum, n8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
+                (e = cudaMemcpyAsync(host_out.sumsq, dst.sumsq, 2 * n8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+                return cuda_fail(e, "cwc_simulate_host: stats download");
+        }
+    }
+    return CWC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cwc_status cwc_model_create(const cwc_model_desc *desc, cwc_model *out) {
+    if (!out) return fail(CWC_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    cwc_model_s *m = new (std::nothrow) cwc_model_s();
+    if (!m) return fail(CWC_ERR_NOMEM, "host allocation");
+    cwc_status s = build_model(desc, m);
+    if (s != CWC_OK) {
+        delete m;
+        return s;
+    }
+    *out = m;
+    g_err.clear();
+    return CWC_OK;
+}
+
+void cwc_model_destroy(cwc_model model) { delete model; }
+
+cwc_status cwc_model_info_get(cwc_model m, cwc_model_info *info) {
+    if (!m || !info) return fail(CWC_ERR_INVALID, "NULL argument");
+    info->n_cells = m->n_cells;
+    info->n_reactions = m->M;
+    info->n_obs = m->n_obs;
+    info->n_rules = m->n_rules;
+    info->path = m->thread_ok ? CWC_PATH_THREAD : CWC_PATH_WARP;
+    info->thread_path_ok = m->thread_ok ? 1 : 0;
+    info->max_deps = m->max_deps;
+    info->n_nu = (int32_t)m->nu_cell.size();
+    info->n_deps = (int64_t)m->dep.size();
+    return CWC_OK;
+}
+
+cwc_status cwc_model_get_flat(cwc_model m, int32_t *entry_rule, int32_t *entry_context, int32_t *entry_child,
+                              int32_t *re_ptr, int32_t *re_cell, int32_t *re_mult, int32_t *nu_ptr, int32_t *nu_cell,
+                              int32_t *nu_delta, int32_t *dep_ptr, int32_t *dep) {
+    if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
+    auto cp = [](int32_t *dst, const std::vector<int32_t> &v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(int32_t));
+    };
+    cp(entry_rule, m->entry_rule);
+    cp(entry_context, m->entry_ctx);
+    cp(entry_child, m->entry_child);
+    cp(re_ptr, m->re_ptr);
+    cp(re_cell, m->re_cell);
+    cp(re_mult, m->re_mult);
+    cp(nu_ptr, m->nu_ptr);
+    cp(nu_cell, m->nu_cell);
+    cp(nu_delta, m->nu_delta);
+    cp(dep_ptr, m->dep_ptr);
+    cp(dep, m->dep);
+    return CWC_OK;
+}
+
+cwc_status cwc_simulate_workspace_size(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                                       double sample_dt, const cwc_sim_opts *opts, size_t *bytes) {
+    if (!bytes) return fail(CWC_ERR_INVALID, "bytes is NULL");
+    Plan pl;
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl);
+    if (s != CWC_OK) return s;
+    *bytes = pl.total;
+    return CWC_OK;
+}
+
+cwc_status cwc_simulate_host_workspace_size(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                                            double sample_dt, size_t *bytes) {
+    if (!bytes) return fail(CWC_ERR_INVALID, "bytes is NULL");
+    Plan pl;
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, nullptr, true, pl);
+    if (s != CWC_OK) return s;
+    *bytes = pl.total;
+    return CWC_OK;
+}
+
+cwc_status cwc_simulate(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                        uint64_t seed, void *cuda_stream, cwc_stats out_stats, void *workspace, size_t workspace_bytes,
+                        const cwc_sim_opts *opts) {
+    return run(m, n_replicas, sweep, t_end, sample_dt, seed, cuda_stream, out_stats, workspace, workspace_bytes, opts,
+               false, cwc_stats{});
+}
+
+cwc_status cwc_simulate_host(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                             uint64_t seed, void *cuda_stream, cwc_stats host_stats, void *workspace,
+                             size_t workspace_bytes) {
+    if (!host_stats.count || !host_stats.sum || !host_stats.sumsq) return fail(CWC_ERR_INVALID, "host stats pointers are NULL");
+    return run(m, n_replicas, sweep, t_end, sample_dt, seed, cuda_stream, host_stats, workspace, workspace_bytes, nullptr,
+               true, host_stats);
+}
+
+cwc_status cwc_stats_finalize(const cwc_stats *stats, int64_t n_cells, double *mean, double *var, double *ci90,
+                              void *cuda_stream) {
+    if (!stats || n_cells < 0) return fail(CWC_ERR_INVALID, "bad arguments");
+    if (n_cells > 0 && (!stats->count || !stats->sum || !stats->sumsq)) return fail(CWC_ERR_INVALID, "stats pointers are NULL");
+    cudaError_t e = launch_stats_finalize(stats->count, stats->sum, stats->sumsq, n_cells, mean, var, ci90,
+                                          (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_stats_finalize");
+    return CWC_OK;
+}
+
+cwc_status cwc_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, uint32_t *out,
+                             void *cuda_stream) {
+    if (count < 0 || (count > 0 && (!g || !n || !out))) return fail(CWC_ERR_INVALID, "bad arguments");
+    cudaError_t e = launch_philox_blocks(seed, g, n, count, out, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_philox_blocks");
+    return CWC_OK;
+}
+
+const char *cwc_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

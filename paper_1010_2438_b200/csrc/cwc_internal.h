@@ -1,0 +1,106 @@
+// cwc_internal.h -- host/device shared layouts of the product path.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "cwc.h"
+
+namespace cwc {
+
+// Thread path limits: cells and reactions live in registers, net change of a
+// reaction is packed as one int8 per cell into a 64-bit word.
+constexpr int kThreadMaxCells = 8;
+constexpr int kThreadMaxReactions = 32;
+constexpr int kThreadMaxObs = 8;
+
+// Reaction encoding shared by both kernels (built by the host compiler):
+// h = xa * (xb - sub) >> shr with xa = x[ia], xb = x[ib] and index
+// "one" (= n_cells, or the padded cell count in the thread path) reading 1.
+struct ReactionDesc {
+    int32_t ia, ib;
+    int32_t kind;   // sub | (shr << 1)
+    int32_t rule;
+};
+
+// RNG key of local trajectory g: point * R_total + r_off + replica.
+__host__ __device__ __forceinline__ int64_t global_traj(int64_t g, int64_t R, int64_t R_total, int64_t r_off) {
+    const int64_t p = g / R;
+    return p * R_total + r_off + (g - p * R);
+}
+
+// Per-launch run description (both kernels).
+struct RunParams {
+    int64_t G;              // trajectories
+    int64_t R;              // replicas per point in this call
+    int64_t R_total;        // replicas per point of the whole (sharded) run
+    int64_t r_off;          // first replica of this call
+    int32_t P;              // points
+    int32_t J;              // last sample index
+    double dt;
+    uint64_t seed;
+    const double *rates;    // [P][M] flat per-reaction rate constants
+    // statistics: accumulator parts (see stats.cu)
+    void *parts;            // n_parts x stat_bytes(cells_per_part)
+    int64_t cells_per_part;
+    int32_t stats_smem;     // 1: block accumulators in shared memory, flushed to parts[blockIdx]
+    int32_t part_stride_blocks;  // GLOBAL mode: block b accumulates into part (b % n_parts)
+    int32_t n_parts;
+    int64_t traj_per_part;  // static mapping: part b covers g in [b*T, (b+1)*T); 0 = all points
+    // optional outputs
+    int64_t *out_traj;
+    int64_t *out_firings;
+    int32_t *out_status;
+    // trace
+    const int64_t *trace_g; // device [n_trace]
+    int32_t n_trace;
+    int64_t trace_cap;
+    double *trace_buf;
+    int64_t *trace_len;
+    // warp path dynamic scheduling
+    unsigned long long *next_traj;
+};
+
+// Thread path tables (kernel parameter, constant bank).
+struct ThreadTables {
+    int32_t n_cells, M, O, pad_;
+    int32_t ia[kThreadMaxReactions], ib[kThreadMaxReactions];
+    int32_t sub[kThreadMaxReactions], shr[kThreadMaxReactions];
+    uint64_t nu_pack[kThreadMaxReactions];   // int8 delta per cell
+    int32_t obs_of[kThreadMaxCells];
+    int32_t init[kThreadMaxCells];
+};
+
+// Warp path tables (device pointers, read through L1).
+struct WarpTables {
+    int32_t n_cells, M, O, B;     // B = reactions per lane chunk = ceil(M / 32)
+    const ReactionDesc *rx;       // [M]
+    const int32_t *nu_ptr;        // [M+1]
+    const int2 *nu;               // (cell, delta)
+    const int32_t *dep_ptr;       // [M+1]
+    const int32_t *dep;
+    const int32_t *obs_ptr;       // [O+1]
+    const int32_t *obs_cells;
+    const int32_t *init;          // [n_cells]
+};
+
+// Launchers (ssa_thread.cu, ssa_warp.cu, stats.cu); return cudaError_t.
+cudaError_t launch_ssa_thread(int s_pad, int m_pad, const RunParams &rp, const ThreadTables &tt, int threads,
+                              size_t smem_bytes, cudaStream_t stream);
+bool thread_variant_exists(int s_pad, int m_pad);
+int thread_pad_cells(int n_cells);
+int thread_pad_reactions(int M);
+
+cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+                            size_t smem_bytes, cudaStream_t stream);
+size_t warp_smem_per_warp(const WarpTables &wt);
+
+cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,
+                                cudaStream_t stream);
+cudaError_t launch_stats_finalize(const int64_t *count, const int64_t *sum, const uint64_t *sumsq, int64_t n,
+                                  double *mean, double *var, double *ci90, cudaStream_t stream);
+cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, uint32_t *out,
+                                 cudaStream_t stream);
+
+}  // namespace cwc

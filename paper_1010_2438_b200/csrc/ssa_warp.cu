@@ -1,0 +1,250 @@
+// ssa_warp.cu -- one trajectory per warp (large networks).
+//
+// Hot path of BASELINE north_star (b): "warp-per-replica for large networks,
+// with a shuffle-scan propensity sum, ballot/ffs reaction selection and
+// dependency-graph propensity updates".  The 32 lanes of a warp share one
+// trajectory -- the GPU form of the intra-step data parallelism the paper
+// applies to Match_Populations with SSE -- and the warps of the
+// grid are a persistent farm that pulls trajectory ids on demand from an
+// atomic counter (schema i, on-demand dispatch).
+//
+// Per warp, in shared memory: counts x[cell] (int32, plus a constant 1 at
+// index n_cells for absent reactants) and propensities a[m] in a
+// lane-chunked layout: lane l owns reactions m in [l*B, (l+1)*B), stored at
+// a[k*32 + l] (bank-conflict free).  Lane l keeps its chunk sum in a
+// register; a Kogge-Stone shuffle scan over the 32 chunk sums gives the
+// inclusive prefixes, a0 = prefix of lane 31.
+//
+// One firing (Fig. fig:simd P:608-621):
+//   tau = E_n / a0 (E_n = -log u1 of Philox block n, drawn 32 at a time: lane
+//   i computes block n_base + i, then broadcast by shuffle), sample crossing
+//   into the block's moment accumulators, target = u2 a0,
+//   L = ffs(ballot(prefix_l > target)), lane L scans its chunk from the
+//   exclusive prefix, x += nu_mu (one lane per changed cell), then only the
+//   reactions in D(mu) are recomputed and only their owner lanes re-sum.
+#include <cuda_runtime.h>
+
+#include "cwc_internal.h"
+#include "device_common.cuh"
+
+namespace cwc {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double shfl_d(double v, int src) { return __shfl_sync(kFull, v, src); }
+
+__device__ __forceinline__ double propensity(const WarpTables &wt, const int *xs, const double *rates, int m) {
+    const int4 d = __ldg(reinterpret_cast<const int4 *>(wt.rx) + m);
+    return __dmul_rn(__ldg(rates + m), combos(xs[d.x], xs[d.y], d.z & 1, d.z >> 1));
+}
+
+// Inclusive Kogge-Stone scan of the 32 chunk sums.
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double y = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v = __dadd_rn(y, v);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
+                                                       int per_warp_bytes, int x_bytes) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int B = wt.B;
+    const int O = wt.O;
+    const int M = wt.M;
+    const long long J = rp.J, J1 = J + 1;
+
+    StatAcc acc;
+    if (rp.stats_smem) {
+        acc = stat_view(smem, rp.cells_per_part);
+        uint4 *z = (uint4 *)smem;
+        for (long long i = threadIdx.x; i < stats_smem_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    } else {
+        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.cells_per_part),
+                        rp.cells_per_part);
+    }
+    int *xs = (int *)(smem + stats_smem_bytes + (long long)wib * per_warp_bytes);
+    double *as = (double *)((unsigned char *)xs + x_bytes);
+    __syncthreads();
+
+    for (;;) {
+        unsigned long long gg = 0;
+        if (lane == 0) gg = atomicAdd(rp.next_traj, 1ull);
+        const long long g = (long long)__shfl_sync(kFull, gg, 0);
+        if (g >= rp.G) break;
+        const long long p = g / rp.R;
+        const double *rates = rp.rates + p * M;
+        const long long cell_base = p * J1 * O;
+        const uint64_t gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);  // RNG stream id
+
+        int tslot = -1;
+        for (int i = 0; i < rp.n_trace; ++i)
+            if (rp.trace_g[i] == g) tslot = i;
+        double *trace = (tslot >= 0) ? rp.trace_buf + (long long)tslot * rp.trace_cap * 5 : nullptr;
+        long long tn_rec = 0;
+
+        for (int c = lane; c < wt.n_cells; c += 32) xs[c] = __ldg(wt.init + c);
+        if (lane == 0) xs[wt.n_cells] = 1;
+        __syncwarp();
+
+        double part = 0.0;
+        for (int k = 0; k < B; ++k) {
+            const int m = lane * B + k;
+            const double a = (m < M) ? propensity(wt, xs, rates, m) : 0.0;
+            as[k * 32 + lane] = a;
+            part = (k == 0) ? a : __dadd_rn(part, a);
+        }
+        double incl = warp_incl_scan(part, lane);
+        double a0 = shfl_d(incl, 31);
+        double excl = __shfl_up_sync(kFull, incl, 1);
+        if (lane == 0) excl = 0.0;
+
+        auto record = [&](long long j) {
+            for (int o = lane; o < O; o += 32) {
+                long long v = 0;
+                for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xs[__ldg(wt.obs_cells + q)];
+                stat_record(acc, cell_base + j * O + o, v);
+                if (rp.out_traj) rp.out_traj[(g * J1 + j) * O + o] = v;
+            }
+        };
+        auto trace_rec = [&](unsigned long long n, double a0_, double tau, double tn, int mu) {
+            if (tslot >= 0 && lane == 0 && tn_rec < rp.trace_cap) {
+                double *r = trace + 5 * tn_rec;
+                r[0] = (double)n; r[1] = a0_; r[2] = tau; r[3] = tn; r[4] = (double)mu;
+            }
+            if (tslot >= 0 && tn_rec < rp.trace_cap) ++tn_rec;
+        };
+
+        double t = 0.0, t_next = 0.0;
+        long long j = 0, firings = 0;
+        unsigned long long n = 0, n_base = 0;
+        int status = CWC_TRAJ_DONE;
+        double El, u2l;
+        block_to_draws(philox_block(rp.seed, gk, (uint64_t)lane), El, u2l);
+
+        for (;;) {
+            if (n - n_base == 32) {
+                n_base = n;
+                block_to_draws(philox_block(rp.seed, gk, n_base + lane), El, u2l);
+            }
+            const int i = (int)(n - n_base);
+            const double E = shfl_d(El, i);
+            const double u2 = shfl_d(u2l, i);
+            const double tau = __ddiv_rn(E, a0);
+            const double tn = __dadd_rn(t, tau);
+            if (!(tn < t_next)) {
+                if (a0 == 0.0) {
+                    for (; j <= J; ++j) record(j);
+                    status = CWC_TRAJ_STALLED;
+                    break;
+                }
+                while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                    record(j);
+                    ++j;
+                }
+                if (j > J) {
+                    trace_rec(n, a0, tau, tn, -1);
+                    status = CWC_TRAJ_DONE;
+                    break;
+                }
+                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+            }
+            const double target = __dmul_rn(u2, a0);
+            const unsigned mask = __ballot_sync(kFull, incl > target);
+            const int L = __ffs(mask) - 1;  // mask != 0: prefix of lane 31 is a0 > target
+            int mu = -1;
+            if (lane == L) {
+                double c = excl;
+                int last_pos = -1;
+                for (int k = 0; k < B; ++k) {
+                    const double a = as[k * 32 + L];
+                    c = __dadd_rn(c, a);
+                    if (a > 0.0) last_pos = k;
+                    if (target < c) { mu = L * B + k; break; }
+                }
+                // the chunk's own left-to-right sum may round below the scanned prefix
+                if (mu < 0) mu = L * B + last_pos;
+            }
+            mu = __shfl_sync(kFull, mu, L);
+            trace_rec(n, a0, tau, tn, mu);
+
+            // Update: one lane per changed cell; distinct cells.
+            const int nb = __ldg(wt.nu_ptr + mu), ne = __ldg(wt.nu_ptr + mu + 1);
+            int2 e = make_int2(0, 0);
+            long long nv = 0;
+            if (lane < ne - nb) {
+                e = __ldg(wt.nu + nb + lane);
+                nv = (long long)xs[e.x] + e.y;
+            }
+            if (__any_sync(kFull, nv > 0x7fffffffll)) {  // a count would leave int32: freeze
+                for (; j <= J; ++j) record(j);
+                status = CWC_TRAJ_OVERFLOW;
+                break;
+            }
+            if (lane < ne - nb) xs[e.x] = (int)nv;
+            __syncwarp();
+
+            // Dependency-graph update: recompute a_m for m in D(mu) only.
+            unsigned dirty = 0;
+            const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
+            for (int q = db + lane; q < de; q += 32) {
+                const int m = __ldg(wt.dep + q);
+                const int owner = m / B, k = m - owner * B;
+                as[k * 32 + owner] = propensity(wt, xs, rates, m);
+                dirty |= 1u << owner;
+            }
+            dirty = __reduce_or_sync(kFull, dirty);
+            __syncwarp();
+            if ((dirty >> lane) & 1u) {
+                double s = as[lane];
+                for (int k = 1; k < B; ++k) s = __dadd_rn(s, as[k * 32 + lane]);
+                part = s;
+            }
+            incl = warp_incl_scan(part, lane);
+            a0 = shfl_d(incl, 31);
+            excl = __shfl_up_sync(kFull, incl, 1);
+            if (lane == 0) excl = 0.0;
+
+            t = tn;
+            ++firings;
+            ++n;
+        }
+        if (lane == 0) {
+            if (rp.out_firings) rp.out_firings[g] = firings;
+            if (rp.out_status) rp.out_status[g] = status;
+            if (tslot >= 0) rp.trace_len[tslot] = tn_rec;
+        }
+        __syncwarp();
+    }
+
+    if (rp.stats_smem) {
+        __syncthreads();
+        const long long n16 = stat_bytes(rp.cells_per_part) / 16;
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.cells_per_part));
+        const uint4 *src = (const uint4 *)smem;
+        for (long long q = threadIdx.x; q < n16; q += blockDim.x) dst[q] = src[q];
+    }
+}
+
+static inline int align16(long long v) { return (int)((v + 15) & ~15ll); }
+
+size_t warp_smem_per_warp(const WarpTables &wt) {
+    return (size_t)align16(4ll * (wt.n_cells + 1)) + (size_t)8 * 32 * wt.B;
+}
+
+cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+                            size_t smem_bytes, cudaStream_t stream) {
+    const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.cells_per_part) : 0;
+    const int x_bytes = align16(4ll * (wt.n_cells + 1));
+    const int per_warp = (int)warp_smem_per_warp(wt);
+    cudaError_t e = cudaFuncSetAttribute(ssa_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+    ssa_warp_kernel<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace cwc

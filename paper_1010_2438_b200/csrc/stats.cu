@@ -1,0 +1,146 @@
+// stats.cu -- second stage of the on-line reduction, finalize, Philox hook.
+//
+// Stage 1 (inside the SSA kernels) leaves one partial moment set per part
+// (per CTA, or per CTA slice): [sum u64][sqlo u64][cnt u32][sqhi u32] over
+// the part's cells.  Stage 2 sums, for every (point, sample, observable)
+// cell, the parts that cover its point and writes count / sum / sumsq(128)
+// -- exact integer addition, so the result does not depend on how
+// trajectories were spread over CTAs (SPEC S:513 determinism).
+#include <cuda_runtime.h>
+
+#include "cwc_internal.h"
+#include "device_common.cuh"
+
+namespace cwc {
+
+__global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n_cells, int64_t *count, int64_t *sum,
+                                    uint64_t *sumsq) {
+    const long long JO = (long long)(rp.J + 1) * O;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n_cells;
+         c += (long long)gridDim.x * blockDim.x) {
+        const long long p = c / JO;
+        const long long rest = c - p * JO;
+        long long b0, b1;
+        if (rp.traj_per_part > 0) {
+            b0 = (p * rp.R) / rp.traj_per_part;
+            b1 = ((p + 1) * rp.R - 1) / rp.traj_per_part;
+            if (b1 > rp.n_parts - 1) b1 = rp.n_parts - 1;
+        } else {
+            b0 = 0;
+            b1 = rp.n_parts - 1;
+        }
+        unsigned long long cnt = 0, s1 = 0;
+        unsigned __int128 s2 = 0;
+        for (long long b = b0; b <= b1; ++b) {
+            long long local = c;
+            if (rp.traj_per_part > 0) local = (p - (b * rp.traj_per_part) / rp.R) * JO + rest;
+            const StatAcc a = stat_view((unsigned char *)rp.parts + b * stat_bytes(rp.cells_per_part), rp.cells_per_part);
+            cnt += a.cnt[local];
+            s1 += a.sum[local];
+            s2 += (unsigned __int128)a.sqlo[local] + ((unsigned __int128)a.sqhi[local] << 64);
+        }
+        count[c] = (int64_t)cnt;
+        sum[c] = (int64_t)s1;
+        sumsq[2 * c] = (uint64_t)s2;
+        sumsq[2 * c + 1] = (uint64_t)(s2 >> 64);
+    }
+}
+
+cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,
+                                cudaStream_t stream) {
+    const long long n_cells = (long long)rp.P * (rp.J + 1) * O;
+    if (n_cells == 0) return cudaSuccess;
+    long long blocks = (n_cells + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    stats_stage2_kernel<<<(unsigned)blocks, 256, 0, stream>>>(rp, O, n_cells, count, sum, sumsq);
+    return cudaGetLastError();
+}
+
+// ---- finalize ---------------------------------------------------------------
+// 192-bit unsigned helpers for n * S2 - S1^2 (n < 2^63, S2 < 2^128, S1 < 2^64).
+struct U192 {
+    unsigned long long w[3];
+};
+
+__device__ __forceinline__ U192 mul_64x128(unsigned long long a, unsigned __int128 b) {
+    const unsigned long long b0 = (unsigned long long)b, b1 = (unsigned long long)(b >> 64);
+    const unsigned __int128 p0 = (unsigned __int128)a * b0;
+    const unsigned __int128 p1 = (unsigned __int128)a * b1 + (p0 >> 64);
+    U192 r;
+    r.w[0] = (unsigned long long)p0;
+    r.w[1] = (unsigned long long)p1;
+    r.w[2] = (unsigned long long)(p1 >> 64);
+    return r;
+}
+
+__device__ __forceinline__ U192 sub_192_128(U192 a, unsigned __int128 b) {
+    const unsigned long long b0 = (unsigned long long)b, b1 = (unsigned long long)(b >> 64);
+    U192 r;
+    r.w[0] = a.w[0] - b0;
+    unsigned long long br = (a.w[0] < b0) ? 1ull : 0ull;
+    const unsigned long long t1 = a.w[1] - b1;
+    const unsigned long long br1 = (a.w[1] < b1) ? 1ull : 0ull;
+    r.w[1] = t1 - br;
+    br = br1 | ((t1 < br) ? 1ull : 0ull);
+    r.w[2] = a.w[2] - br;
+    return r;
+}
+
+__device__ __forceinline__ double u192_to_double(U192 a) {
+    // exact scaling by powers of two; the sum rounds once per term
+    return __dadd_rn(__dadd_rn(__dmul_rn(__ull2double_rn(a.w[2]), 0x1.0p128), __dmul_rn(__ull2double_rn(a.w[1]), 0x1.0p64)),
+                     __ull2double_rn(a.w[0]));
+}
+
+__global__ void stats_finalize_kernel(const int64_t *count, const int64_t *sum, const uint64_t *sumsq, long long n,
+                                      double *mean, double *var, double *ci90) {
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        const long long cnt = count[c];
+        const unsigned long long s1 = (unsigned long long)sum[c];
+        const unsigned __int128 s2 = (unsigned __int128)sumsq[2 * c] | ((unsigned __int128)sumsq[2 * c + 1] << 64);
+        double m = __longlong_as_double(0x7ff8000000000000ll), v = m, ci = m;
+        if (cnt > 0) {
+            m = __ddiv_rn(__ull2double_rn(s1), __ll2double_rn(cnt));
+            if (cnt == 1) {
+                v = 0.0;
+                ci = 0.0;
+            } else {
+                const U192 num = sub_192_128(mul_64x128((unsigned long long)cnt, s2), (unsigned __int128)s1 * s1);
+                const double den = __dmul_rn(__ll2double_rn(cnt), __ll2double_rn(cnt - 1));
+                v = __ddiv_rn(u192_to_double(num), den);
+                ci = __dmul_rn(1.6449, sqrt(__ddiv_rn(v, __ll2double_rn(cnt))));
+            }
+        }
+        if (mean) mean[c] = m;
+        if (var) var[c] = v;
+        if (ci90) ci90[c] = ci;
+    }
+}
+
+cudaError_t launch_stats_finalize(const int64_t *count, const int64_t *sum, const uint64_t *sumsq, int64_t n,
+                                  double *mean, double *var, double *ci90, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    stats_finalize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(count, sum, sumsq, n, mean, var, ci90);
+    return cudaGetLastError();
+}
+
+// ---- Philox hook -------------------------------------------------------------
+__global__ void philox_blocks_kernel(uint64_t seed, const int64_t *g, const int64_t *n, long long count, uint32_t *out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+        const uint4 w = philox_block(seed, (uint64_t)g[i], (uint64_t)n[i]);
+        reinterpret_cast<uint4 *>(out)[i] = w;
+    }
+}
+
+cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, uint32_t *out,
+                                 cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    long long blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    philox_blocks_kernel<<<(unsigned)blocks, 256, 0, stream>>>(seed, g, n, count, out);
+    return cudaGetLastError();
+}
+
+}  // namespace cwc

@@ -1,0 +1,156 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol cwc.h
+declares, and its host logic (validation, flattening, dependency graph,
+launch planning) is correct.  No kernel is launched here (no GPU)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+from paper_1010_2438_b200 import cwc
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_1010_2438_b200 import _build
+    _build.build()
+
+
+def test_every_declared_symbol_is_exported():
+    hdr = open(os.path.join(ROOT, "include", "cwc.h")).read()
+    declared = set(re.findall(r"\b(cwc_[a-z0-9_]+)\s*\(", hdr))
+    assert "cwc_simulate" in declared and "cwc_model_create" in declared
+    L = cwc.lib()
+    for name in sorted(declared):
+        assert hasattr(L, name), name
+    assert set(cwc.EXPORTED) == declared
+
+
+MODELS = [("paper", lambda: w.paper_example_model()), ("small_cwc", lambda: w.small_cwc_model(3, 1)),
+          ("C1", lambda: w.config("C1")[0]), ("C2", lambda: w.config("C2")[0]), ("C3", lambda: w.config("C3")[0]),
+          ("C4", lambda: w.config("C4")[0]), ("C5", lambda: w.config("C5")[0]),
+          ("dimer", lambda: w.dimerisation_model())]
+
+
+@pytest.mark.parametrize("name,make", MODELS)
+def test_flattening_equals_oracle_flattening(name, make):
+    d = make()
+    m = cwc.cwc_model_create(d)
+    f = m.get_flat()
+    ent = oracle.flatten(d)
+    assert m.info.n_reactions == len(ent)
+    assert list(f["entry_rule"]) == [e["rule"] for e in ent]
+    assert list(f["entry_context"]) == [e["context"] for e in ent]
+    assert list(f["entry_child"]) == [e["child"] for e in ent]
+    for k, e in enumerate(ent):
+        lo, hi = f["re_ptr"][k], f["re_ptr"][k + 1]
+        assert list(zip(f["re_cell"][lo:hi], f["re_mult"][lo:hi])) == [tuple(x) for x in e["reactants"]]
+        lo, hi = f["nu_ptr"][k], f["nu_ptr"][k + 1]
+        assert list(zip(f["nu_cell"][lo:hi], f["nu_delta"][lo:hi])) == [tuple(x) for x in e["nu"]]
+
+
+@pytest.mark.parametrize("name,make", MODELS)
+def test_dependency_graph_is_exact(name, make):
+    d = make()
+    m = cwc.cwc_model_create(d)
+    f = m.get_flat()
+    ent = oracle.flatten(d)
+    reads = [set(c for c, _ in e["reactants"]) for e in ent]
+    for mu, e in enumerate(ent):
+        changed = set(c for c, _ in e["nu"])
+        want = [k for k in range(len(ent)) if reads[k] & changed]
+        got = list(f["dep"][f["dep_ptr"][mu]:f["dep_ptr"][mu + 1]])
+        assert got == want, mu
+    assert m.info.max_deps == max((f["dep_ptr"][i + 1] - f["dep_ptr"][i] for i in range(len(ent))), default=0)
+
+
+def test_path_choice():
+    assert cwc.cwc_model_create(w.config("C2")[0]).info.path == cwc.CWC_PATH_THREAD
+    assert cwc.cwc_model_create(w.config("C3")[0]).info.path == cwc.CWC_PATH_THREAD
+    assert cwc.cwc_model_create(w.config("C4")[0]).info.path == cwc.CWC_PATH_WARP
+    assert cwc.cwc_model_create(w.config("C5")[0]).info.path == cwc.CWC_PATH_WARP
+
+
+def _bad(mut):
+    d = w.lotka_volterra_model()
+    mut(d)
+    with pytest.raises(cwc.CwcError) as ei:
+        cwc.cwc_model_create(d)
+    return ei.value.status
+
+
+def test_model_validation_errors():
+    R = w.models._rule
+    assert _bad(lambda d: d["rules"][0].__setitem__("rate", 0.0)) == cwc.CWC_ERR_INVALID
+    assert _bad(lambda d: d["rules"][0].__setitem__("rate", float("nan"))) == cwc.CWC_ERR_INVALID
+    assert _bad(lambda d: d["rules"][0].__setitem__("rate", float("inf"))) == cwc.CWC_ERR_INVALID
+    assert _bad(lambda d: d["init"].__setitem__(0, -1)) == cwc.CWC_ERR_INVALID
+    assert _bad(lambda d: d["rules"].append(R(0, [(0, 0, 3)], [], 1.0))) == cwc.CWC_ERR_UNSUPPORTED
+    assert _bad(lambda d: d["rules"].append(R(0, [(0, 0, 2), (0, 1, 1)], [], 1.0))) == cwc.CWC_ERR_UNSUPPORTED
+    assert _bad(lambda d: d["rules"].append(R(0, [(1, 0, 1)], [], 1.0))) == cwc.CWC_ERR_INVALID  # child on local rule
+    assert _bad(lambda d: d["rules"].append(R(0, [(0, 5, 1)], [], 1.0))) == cwc.CWC_ERR_INVALID  # species range
+    assert _bad(lambda d: d["rules"].append(R(3, [], [], 1.0))) == cwc.CWC_ERR_INVALID  # label range
+    assert _bad(lambda d: d["rules"].append(R(0, [(0, 0, 0)], [], 1.0))) == cwc.CWC_ERR_INVALID  # mult 0
+    assert _bad(lambda d: d["obs_of_cell"].__setitem__(0, 7)) == cwc.CWC_ERR_INVALID
+
+
+def test_tree_validation_errors():
+    d = w.small_cwc_model(2)
+    d["parent"][2] = 3  # parent index not < child index
+    with pytest.raises(cwc.CwcError):
+        cwc.cwc_model_create(d)
+    d = w.small_cwc_model(2)
+    d["type"][0] = 1
+    with pytest.raises(cwc.CwcError):
+        cwc.cwc_model_create(d)
+    d = w.small_cwc_model(2)
+    d["type"][1] = 9
+    with pytest.raises(cwc.CwcError):
+        cwc.cwc_model_create(d)
+
+
+def test_run_argument_errors():
+    m = cwc.cwc_model_create(w.config("C2")[0])
+    for args in [(16, None, 0.0, 0.1), (16, None, -1.0, 0.1), (16, None, 1.0, 0.0), (16, None, 1.0, 2.0),
+                 (0, None, 1.0, 0.1), (16, None, float("inf"), 0.1),
+                 (16, {"rules": [7], "values": [[1.0]]}, 1.0, 0.1),
+                 (16, {"rules": [0], "values": [[-1.0]]}, 1.0, 0.1),
+                 (16, {"rules": [0], "values": []}, 1.0, 0.1)]:
+        with pytest.raises(cwc.CwcError) as ei:
+            cwc.cwc_simulate_workspace_size(m, *args)
+        assert ei.value.status == cwc.CWC_ERR_INVALID, args
+    opts = cwc.cwc_sim_opts()
+    opts.force_path = cwc.CWC_PATH_THREAD
+    big = cwc.cwc_model_create(w.config("C4")[0])
+    with pytest.raises(cwc.CwcError):
+        cwc.cwc_simulate_workspace_size(big, 16, None, 1.0, 0.1, opts)
+    opts.force_path = cwc.CWC_PATH_AUTO
+    opts.block_threads = 48
+    with pytest.raises(cwc.CwcError):
+        cwc.cwc_simulate_workspace_size(m, 16, None, 1.0, 0.1, opts)
+
+
+def test_workspace_grows_with_work():
+    m = cwc.cwc_model_create(w.config("C3")[0])
+    d, sweep, cfg = w.config("C3")
+    a = cwc.cwc_simulate_workspace_size(m, 16, sweep, 50.0, 0.5)
+    b = cwc.cwc_simulate_workspace_size(m, 16, None, 50.0, 0.5)
+    assert a > b > 0
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_simulate_without_gpu_fails_loudly():
+    import torch
+    m = cwc.cwc_model_create(w.config("C1")[0])
+    z = torch.zeros(8, dtype=torch.int64)
+    ws = torch.zeros(1 << 20, dtype=torch.uint8)
+    with pytest.raises(cwc.CwcError) as ei:
+        cwc.cwc_simulate(m, 16, None, 10.0, 1.0, 1, 0, (z, z, z), ws)
+    assert ei.value.status == cwc.CWC_ERR_CUDA
+    with pytest.raises(RuntimeError):
+        cwc.simulate(m, 16, 10.0, 1.0, 1)

@@ -1,0 +1,227 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE north_star): species counts at every sample bit-exact for
+>= 99.9% of trajectories under the same Philox streams, every divergence
+traced (tests/tracer.py) to a last-ulp fp64 log or sum-order difference,
+never to a BUG; merged moments over matched trajectories equal (exact
+integers); mean/variance within 1e-9 relative.  Sizes: small cases the
+oracle runs whole (several CTAs, ragged tails), and BASELINE's full configs
+in the bench launch shape with oracle-sampled trajectories.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import workloads as w  # noqa: E402
+
+from .tracer import trace_mismatches  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1010_2438_b200 import cwc  # noqa: E402
+
+MIN_MATCH = 0.999
+
+
+def _gpu(model, cfg, sweep=None, **kw):
+    out = cwc.simulate(model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep, **kw)
+    torch.cuda.synchronize()
+    return out
+
+
+def _assert_moments_equal_dump(gpu, P, R):
+    """The kernel's on-line moments equal an independent reduction of its own
+    trajectory dump (int64 torch sums on the device: exact, bounds checked)."""
+    t = gpu["traj"].view(P, R, gpu["traj"].shape[1], gpu["traj"].shape[2])
+    vmax = int(t.abs().max().item()) if t.numel() else 0
+    assert vmax * vmax * R < 2**62, "dump too large for exact int64 check"
+    assert (gpu["count"] == R).all()
+    assert torch.equal(gpu["sum"], t.sum(dim=1))
+    assert (gpu["sumsq"][..., 1] == 0).all()
+    assert torch.equal(gpu["sumsq"][..., 0], (t * t).sum(dim=1))
+
+
+def _check_parity(desc, model, cfg, sweep, gpu, g_list, force_path, warp_path):
+    """Compare sampled trajectories with the oracle; trace every mismatch."""
+    ora = oracle.simulate(desc, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep,
+                          g_list=g_list, want_stats=False)
+    gt = gpu["traj"][torch.as_tensor(np.asarray(g_list), device="cuda")].cpu().numpy()
+    gf = gpu["firings"][torch.as_tensor(np.asarray(g_list), device="cuda")].cpu().numpy()
+    gs = gpu["status"][torch.as_tensor(np.asarray(g_list), device="cuda")].cpu().numpy()
+    same = np.array([(gt[i] == ora["traj"][i]).all() for i in range(len(g_list))])
+    same &= (gf == ora["firings"]) | ~same
+    bad = [g_list[i] for i in np.nonzero(~same)[0]]
+    report = trace_mismatches(model, desc, sweep, cfg, bad, warp_path, force_path) if bad else []
+    for rec in report:
+        assert rec[1] != "BUG", rec
+    assert same.mean() >= MIN_MATCH, (same.mean(), report)
+    matched = np.nonzero(same)[0]
+    assert (gf[matched] == ora["firings"][matched]).all()
+    assert (gs[matched] == ora["status"][matched]).all()
+    return same, report, ora
+
+
+# ---------------------------------------------------------------------------
+# RNG
+# ---------------------------------------------------------------------------
+
+def test_device_philox_matches_oracle():
+    rng = np.random.default_rng(0)
+    g = rng.integers(0, 2**62, size=4096, dtype=np.int64)
+    n = rng.integers(0, 2**62, size=4096, dtype=np.int64)
+    g[:4] = [0, 1, 2**62 - 1, 16383]
+    n[:4] = [0, 0, 5, 300000]
+    out = torch.zeros((4096, 4), dtype=torch.int32, device="cuda")
+    for seed in (1, 0xFFFFFFFFFFFF1234):
+        cwc.cwc_philox_blocks(seed, torch.as_tensor(g, device="cuda"), torch.as_tensor(n, device="cuda"), out,
+                              torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy().view(np.uint32)
+        for i in range(0, 4096, 37):
+            gi, ni = int(g[i]), int(n[i])
+            want = oracle.philox4x32_10([ni & 0xFFFFFFFF, ni >> 32, gi & 0xFFFFFFFF, gi >> 32],
+                                        [seed & 0xFFFFFFFF, seed >> 32])
+            assert list(got[i]) == want
+
+
+# ---------------------------------------------------------------------------
+# thread path, small sizes: whole oracle, several CTAs + ragged tail
+# ---------------------------------------------------------------------------
+
+SMALL = [
+    ("C1", lambda: (w.config("C1")[0], None), dict(t_end=100.0, sample_dt=1.0, n_replicas=1000, seed=1)),
+    ("C2", lambda: (w.config("C2")[0], None), dict(t_end=2.0, sample_dt=0.01, n_replicas=300, seed=1)),
+    ("C3", lambda: (w.config("C3")[0], w.mm_sweep(5, 7)), dict(t_end=50.0, sample_dt=0.5, n_replicas=13, seed=1)),
+    ("decay", lambda: (w.decay_model(1000, 1.0), None), dict(t_end=1.0, sample_dt=0.25, n_replicas=777, seed=3)),
+    ("stall", lambda: (w.decay_model(3, 5.0), None), dict(t_end=10.0, sample_dt=1.0, n_replicas=65, seed=4)),
+    ("dimer", lambda: (w.dimerisation_model(50, 0.1), None), dict(t_end=3.0, sample_dt=0.1, n_replicas=129, seed=8)),
+    ("paper", lambda: (w.paper_example_model(0.5), None), dict(t_end=5.0, sample_dt=0.5, n_replicas=40, seed=2)),
+    ("one", lambda: (w.config("C1")[0], None), dict(t_end=3.0, sample_dt=3.0, n_replicas=1, seed=5)),
+]
+
+
+@pytest.mark.parametrize("name,make,cfg", SMALL, ids=[s[0] for s in SMALL])
+@pytest.mark.parametrize("path", [cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP])
+def test_small_parity_full_oracle(name, make, cfg, path):
+    desc, sweep = make()
+    model = cwc.cwc_model_create(desc)
+    gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path)
+    P = gpu["n_points"]
+    G = P * cfg["n_replicas"]
+    same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, list(range(G)), path, path == cwc.CWC_PATH_WARP)
+    # moments: GPU on-line stats == reduction of the GPU's own dump (exact)
+    _assert_moments_equal_dump(gpu, P, cfg["n_replicas"])
+    if same.all():  # and == oracle's own on-line moments
+        o = oracle.simulate(desc, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep,
+                            want_traj=False)
+        assert (gpu["count"].cpu().numpy() == o["count"]).all()
+        assert (gpu["sum"].cpu().numpy() == o["sum"]).all()
+        assert (gpu["sumsq"].cpu().numpy().view(np.uint64) == o["sumsq"]).all()
+
+
+def test_overflow_status():
+    desc = w.immigration_death_model(k_in=1e6, k_out=1e-12, a0=2**31 - 5)
+    cfg = dict(t_end=1.0, sample_dt=0.5, n_replicas=40, seed=1)
+    for path in (cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP):
+        gpu = _gpu(cwc.cwc_model_create(desc), cfg, want_traj=True, force_path=path)
+        assert (gpu["status"].cpu().numpy() == cwc.CWC_TRAJ_OVERFLOW).all()
+        assert (gpu["firings"].cpu().numpy() == 4).all()
+        assert (gpu["traj"][:, -1, 0].cpu().numpy() == 2**31 - 1).all()
+
+
+def test_no_rules_stalls_immediately():
+    desc = w.decay_model(5, 1.0)
+    desc["rules"] = []
+    cfg = dict(t_end=2.0, sample_dt=0.5, n_replicas=33, seed=1)
+    for path in (cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP):
+        gpu = _gpu(cwc.cwc_model_create(desc), cfg, want_traj=True, force_path=path)
+        assert (gpu["status"].cpu().numpy() == cwc.CWC_TRAJ_STALLED).all()
+        assert (gpu["traj"].cpu().numpy() == 5).all()
+        assert (gpu["count"].cpu().numpy() == 33).all()
+
+
+@pytest.mark.parametrize("bt", [32, 64, 96, 160, 256])
+def test_launch_shape_does_not_change_results(bt):
+    desc, _, _ = w.config("C2")
+    cfg = dict(t_end=1.0, sample_dt=0.01, n_replicas=1111, seed=7)
+    model = cwc.cwc_model_create(desc)
+    ref = _gpu(model, cfg, block_threads=0)
+    got = _gpu(model, cfg, block_threads=bt)
+    for k in ("count", "sum", "sumsq", "firings", "status"):
+        assert torch.equal(ref[k], got[k]), k
+
+
+@pytest.mark.parametrize("mode", ["smem", "global"])
+def test_stats_modes_agree(mode, monkeypatch):
+    desc, sweep, _ = w.config("C3")
+    sweep = w.mm_sweep(6, 6)
+    cfg = dict(t_end=20.0, sample_dt=0.5, n_replicas=40, seed=1)
+    model = cwc.cwc_model_create(desc)
+    ref = _gpu(model, cfg, sweep)
+    monkeypatch.setenv("CWC_STATS_MODE", mode)
+    for path in (cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP):
+        got = _gpu(model, cfg, sweep, force_path=path)
+        for k in ("count", "sum", "sumsq"):
+            assert torch.equal(ref[k], got[k]), (mode, path, k)
+
+
+def test_finalize_matches_oracle_moments():
+    desc, _, _ = w.config("C1")
+    cfg = dict(t_end=100.0, sample_dt=1.0, n_replicas=1024, seed=1)
+    gpu = _gpu(cwc.cwc_model_create(desc), cfg, finalize=True)
+    o = oracle.simulate(desc, 1024, 100.0, 1.0, 1, want_traj=False)
+    means, vars_, cis = oracle.finalize(o["count"], o["sum"], o["sumsq"])
+    for got, want in ((gpu["mean"], means), (gpu["var"], vars_), (gpu["ci90"], cis)):
+        g = got.cpu().numpy().reshape(-1)
+        wv = np.asarray(want)
+        assert np.all(np.abs(g - wv) <= 1e-9 * np.maximum(np.abs(g), np.abs(wv)))
+
+
+def test_trace_equals_oracle_trace_thread_path():
+    desc, _, _ = w.config("C2")
+    cfg = dict(t_end=0.5, sample_dt=0.01, n_replicas=64, seed=1)
+    model = cwc.cwc_model_create(desc)
+    rep = trace_mismatches(model, desc, None, cfg, [0, 17, 63], False, cwc.CWC_PATH_THREAD)
+    for g, cat, idx, detail in rep:
+        assert cat in ("identical-trace", "log-ulp"), (g, cat, idx, detail)
+
+
+# ---------------------------------------------------------------------------
+# full BASELINE configs, bench launch shape, oracle-sampled trajectories
+# ---------------------------------------------------------------------------
+
+FULL = [("C1", 1), ("C2", 512), ("C3", 1024), ("C4", 2048), ("C5", 2048)]
+
+
+@pytest.mark.parametrize("name,stride", FULL, ids=[f[0] for f in FULL])
+def test_full_config_sampled_parity(name, stride):
+    desc, sweep, cfg = w.config(name)
+    model = cwc.cwc_model_create(desc)
+    warp = model.info.path == cwc.CWC_PATH_WARP
+    gpu = _gpu(model, cfg, sweep, want_traj=True)
+    bench_like = _gpu(model, cfg, sweep, want_firings=False)  # the exact call bench.py times
+    for k in ("count", "sum", "sumsq"):
+        assert torch.equal(gpu[k], bench_like[k]), k
+    P = gpu["n_points"]
+    G = P * cfg["n_replicas"]
+    assert (gpu["status"].cpu().numpy() == cwc.CWC_TRAJ_DONE).all()
+    # exact on-line moments == reduction of the dump (every trajectory)
+    _assert_moments_equal_dump(gpu, P, cfg["n_replicas"])
+    # sampled trajectories vs the oracle (first, last, ragged stride)
+    g_list = sorted(set(list(range(0, G, stride)) + [G - 1]))
+    same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, g_list, cwc.CWC_PATH_AUTO, warp)
+    # moments over the matched sample, mean / variance per sample time within 1e-9
+    idx = np.nonzero(same)[0]
+    a = gpu["traj"][torch.as_tensor(np.asarray(g_list)[idx], device="cuda")].cpu().numpy().astype(np.float64)
+    b = ora["traj"][idx].astype(np.float64)
+    assert np.allclose(a.mean(axis=0), b.mean(axis=0), rtol=1e-9, atol=0)
+    if len(idx) > 1:
+        assert np.allclose(a.var(axis=0, ddof=1), b.var(axis=0, ddof=1), rtol=1e-9, atol=1e-12)
