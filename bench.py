@@ -67,7 +67,7 @@ class ClockSampler:
     def __init__(self, device_index):
         self.dev = device_index
         self.proc = None
-        self.path = os.path.join("/tmp", "cwc_clocks_%d_%d.csv" % (os.getpid(), device_index))
+        self.path = os.path.join("/tmp", "cwc_clocks_%d_%s.csv" % (os.getpid(), device_index))
 
     def start(self):
         try:

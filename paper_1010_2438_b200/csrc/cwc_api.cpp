@@ -216,6 +216,12 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
         m->obs_ptr[o + 1] = (int32_t)m->obs_cells.size();
     }
 
+    // warp path sizes (pointers are filled by upload)
+    m->wt.n_cells = m->n_cells;
+    m->wt.M = m->M;
+    m->wt.O = m->n_obs;
+    m->wt.B = std::max(1, (m->M + 31) / 32);
+
     // thread path tables
     bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
     for (size_t q = 0; ok && q < m->nu_delta.size(); ++q)
@@ -277,10 +283,6 @@ cwc_status upload(cwc_model_s *m) {
     if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaMemcpy");
     unsigned char *b = (unsigned char *)m->dev.p;
     WarpTables &w = m->wt;
-    w.n_cells = m->n_cells;
-    w.M = m->M;
-    w.O = m->n_obs;
-    w.B = std::max(1, (m->M + 31) / 32);
     w.rx = (const ReactionDesc *)(b + o_rx);
     w.nu_ptr = (const int32_t *)(b + o_nup);
     w.nu = (const int2 *)(b + o_nu);
@@ -388,23 +390,23 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             np_max = std::max(np_max, plst - pf + 1);
             if (np_max >= pl.P) break;
         }
-        const int64_t cells = ((np_max * J1 * O) + 1) & ~int64_t(1);
-        const size_t smem = (size_t)(24 * cells);
+        const int64_t cells = stat_cells_round(np_max * J1 * O);
+        const size_t smem = (size_t)stat_bytes(cells);
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
         bool use_smem = smem <= smem_cap && (int64_t)smem * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
         if (O == 0) use_smem = false;
         if (use_smem) {
             pl.stats_smem = 1;
-            pl.cells_per_part = std::max<int64_t>(cells, 2);
+            pl.cells_per_part = std::max<int64_t>(cells, 4);
             pl.n_parts = pl.blocks;
             pl.traj_per_part = T;
             pl.smem_bytes = smem;
         } else {
             pl.stats_smem = 0;
-            pl.cells_per_part = std::max<int64_t>((pl.n_stat_cells + 1) & ~int64_t(1), 2);
+            pl.cells_per_part = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
             const int64_t budget = (int64_t)256 << 20;
-            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / (24 * pl.cells_per_part)));
+            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / stat_bytes(pl.cells_per_part)));
             pl.n_parts = (int)np;
             pl.traj_per_part = 0;
             pl.smem_bytes = 0;
@@ -415,8 +417,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
         pl.warps_per_block = W;
         const size_t per_warp = warp_smem_per_warp(w);
-        const int64_t cells = std::max<int64_t>((pl.n_stat_cells + 1) & ~int64_t(1), 2);
-        const size_t stats = (size_t)(24 * cells);
+        const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
+        const size_t stats = (size_t)stat_bytes(cells);
         bool use_smem = stats + W * per_warp <= 96 * 1024;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
         if (O == 0) use_smem = false;
@@ -440,7 +442,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             pl.n_parts = pl.blocks;
         } else {
             const int64_t budget = (int64_t)512 << 20;
-            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / (24 * cells)));
+            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / stat_bytes(cells)));
         }
     }
 
@@ -449,7 +451,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     pl.off_rates = off;
     off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
     pl.off_parts = off;
-    off = align256(off + (size_t)24 * pl.cells_per_part * pl.n_parts);
+    off = align256(off + (size_t)stat_bytes(pl.cells_per_part) * pl.n_parts);
     pl.off_trace = off;
     off = align256(off + sizeof(int64_t) * (size_t)std::max(opts ? opts->n_trace : 0, 1));
     pl.off_counter = off;
@@ -532,7 +534,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         }
     }
     if (!pl.stats_smem) {
-        e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)24 * pl.cells_per_part * pl.n_parts, stream);
+        e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)stat_bytes(pl.cells_per_part) * pl.n_parts, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: zero partials");
     }
     e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);

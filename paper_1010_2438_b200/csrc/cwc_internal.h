@@ -24,6 +24,12 @@ struct ReactionDesc {
     int32_t rule;
 };
 
+// Statistics accumulator layout (device_common.cuh): kStatWords u32 word
+// arrays of n cells each (n a multiple of 4 so every part is 16-byte sized).
+constexpr int kStatWords = 7;
+__host__ __device__ __forceinline__ long long stat_bytes(long long n) { return 4ll * kStatWords * n; }
+__host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }
+
 // RNG key of local trajectory g: point * R_total + r_off + replica.
 __host__ __device__ __forceinline__ int64_t global_traj(int64_t g, int64_t R, int64_t R_total, int64_t r_off) {
     const int64_t p = g / R;

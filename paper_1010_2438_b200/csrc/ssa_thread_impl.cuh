@@ -58,14 +58,18 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
                         rp.cells_per_part);
     }
 
-    if (g < rp.G) {
-        const long long p = g / rp.R;
+    // Lanes past the last trajectory stay in the warp-uniform loop as idle
+    // lanes (their loads use a valid trajectory id; they never record).
+    const bool in_range = g < rp.G;
+    const long long gc = in_range ? g : rp.G - 1;
+    {
+        const long long p = gc / rp.R;
         const long long cell_base = (p - p_base) * J1 * O;
-        const uint64_t gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);  // RNG stream id
+        const uint64_t gk = (uint64_t)global_traj(gc, rp.R, rp.R_total, rp.r_off);  // RNG stream id
         int tslot = -1;
         double *trace = nullptr;
         long long tn_rec = 0;
-        if (TRACE) {
+        if (TRACE && in_range) {
             for (int i = 0; i < rp.n_trace; ++i)
                 if (rp.trace_g[i] == g) tslot = i;
             if (tslot >= 0) trace = rp.trace_buf + (long long)tslot * rp.trace_cap * 5;
@@ -101,7 +105,13 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
         double E, u2;
         block_to_draws(philox_block(rp.seed, gk, 0), E, u2);
 
-        for (;;) {
+        // Warp-uniform loop: every iteration reconverges at the vote, so the
+        // lanes of a warp advance their trajectories in lock-step and a lane
+        // that takes the rare path (crossing / end / stall) costs the others
+        // one short wait instead of splitting the warp for good.
+        bool live = in_range;
+        while (__any_sync(0xffffffffu, live)) {
+            if (!live) continue;
             double cum[M];
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -116,54 +126,62 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
             double E1, u21;
             block_to_draws(philox_block(rp.seed, gk, n + 1), E1, u21);
 
+            bool apply = true;
             if (!(tn < t_next)) {  // rare: sample crossing, end of horizon, or stall
                 if (a0 == 0.0) {
                     for (; j <= J; ++j) record(j);
                     status = CWC_TRAJ_STALLED;
-                    break;
+                    live = apply = false;
+                } else {
+                    while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                        record(j);
+                        ++j;
+                    }
+                    if (j > J) {
+                        trace_rec(n, a0, tau, tn, -1);
+                        status = CWC_TRAJ_DONE;
+                        live = apply = false;
+                    } else {
+                        t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                    }
                 }
-                while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
-                    record(j);
-                    ++j;
+            }
+            if (apply) {
+                unsigned long long nu = tt.nu_pack[0];
+#pragma unroll
+                for (int m = 0; m + 1 < M; ++m) nu = (cum[m] <= target) ? tt.nu_pack[m + 1] : nu;
+                if (TRACE && tslot >= 0) {
+                    int mu = 0;
+#pragma unroll
+                    for (int m = 0; m + 1 < M; ++m) mu += (cum[m] <= target) ? 1 : 0;
+                    trace_rec(n, a0, tau, tn, mu);
                 }
-                if (j > J) {
-                    trace_rec(n, a0, tau, tn, -1);
-                    status = CWC_TRAJ_DONE;
-                    break;
+                bool wrapped = false;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    x[s] += (int)(signed char)(unsigned char)(nu >> (8 * s));
+                    wrapped |= (x[s] < 0);
                 }
-                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
-            }
-            unsigned long long nu = tt.nu_pack[0];
+                if (wrapped) {  // a count left int32: undo, freeze, fill
 #pragma unroll
-            for (int m = 0; m + 1 < M; ++m) nu = (cum[m] <= target) ? tt.nu_pack[m + 1] : nu;
-            if (TRACE && tslot >= 0) {
-                int mu = 0;
-#pragma unroll
-                for (int m = 0; m + 1 < M; ++m) mu += (cum[m] <= target) ? 1 : 0;
-                trace_rec(n, a0, tau, tn, mu);
+                    for (int s = 0; s < S; ++s) x[s] -= (int)(signed char)(unsigned char)(nu >> (8 * s));
+                    for (; j <= J; ++j) record(j);
+                    status = CWC_TRAJ_OVERFLOW;
+                    live = false;
+                } else {
+                    t = tn;
+                    ++firings;
+                    ++n;
+                    E = E1;
+                    u2 = u21;
+                }
             }
-            bool wrapped = false;
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                x[s] += (int)(signed char)(unsigned char)(nu >> (8 * s));
-                wrapped |= (x[s] < 0);
-            }
-            if (wrapped) {  // a count left int32: undo, freeze, fill
-#pragma unroll
-                for (int s = 0; s < S; ++s) x[s] -= (int)(signed char)(unsigned char)(nu >> (8 * s));
-                for (; j <= J; ++j) record(j);
-                status = CWC_TRAJ_OVERFLOW;
-                break;
-            }
-            t = tn;
-            ++firings;
-            ++n;
-            E = E1;
-            u2 = u21;
         }
-        if (rp.out_firings) rp.out_firings[g] = firings;
-        if (rp.out_status) rp.out_status[g] = status;
-        if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
+        if (in_range) {
+            if (rp.out_firings) rp.out_firings[g] = firings;
+            if (rp.out_status) rp.out_status[g] = status;
+            if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
+        }
     }
 
     if (rp.stats_smem) {  // coalesced, vectorised flush of the block's partial moments

@@ -1,8 +1,8 @@
 // stats.cu -- second stage of the on-line reduction, finalize, Philox hook.
 //
 // Stage 1 (inside the SSA kernels) leaves one partial moment set per part
-// (per CTA, or per CTA slice): [sum u64][sqlo u64][cnt u32][sqhi u32] over
-// the part's cells.  Stage 2 sums, for every (point, sample, observable)
+// (per CTA, or per CTA slice): 7 little-endian u32 word arrays over the
+// part's cells (count; sum lo/hi; sumsq w0..w3).  Stage 2 sums, for every (point, sample, observable)
 // cell, the parts that cover its point and writes count / sum / sumsq(128)
 // -- exact integer addition, so the result does not depend on how
 // trajectories were spread over CTAs (SPEC S:513 determinism).
@@ -35,9 +35,10 @@ __global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n
             long long local = c;
             if (rp.traj_per_part > 0) local = (p - (b * rp.traj_per_part) / rp.R) * JO + rest;
             const StatAcc a = stat_view((unsigned char *)rp.parts + b * stat_bytes(rp.cells_per_part), rp.cells_per_part);
-            cnt += a.cnt[local];
-            s1 += a.sum[local];
-            s2 += (unsigned __int128)a.sqlo[local] + ((unsigned __int128)a.sqhi[local] << 64);
+            cnt += a.w[0][local];
+            s1 += (unsigned long long)a.w[1][local] | ((unsigned long long)a.w[2][local] << 32);
+            s2 += (unsigned __int128)((unsigned long long)a.w[3][local] | ((unsigned long long)a.w[4][local] << 32)) +
+                  ((unsigned __int128)((unsigned long long)a.w[5][local] | ((unsigned long long)a.w[6][local] << 32)) << 64);
         }
         count[c] = (int64_t)cnt;
         sum[c] = (int64_t)s1;

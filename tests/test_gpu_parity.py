@@ -212,7 +212,8 @@ def test_full_config_sampled_parity(name, stride):
         assert torch.equal(gpu[k], bench_like[k]), k
     P = gpu["n_points"]
     G = P * cfg["n_replicas"]
-    assert (gpu["status"].cpu().numpy() == cwc.CWC_TRAJ_DONE).all()
+    # MM trajectories that convert all substrate stall legitimately (a0 = 0)
+    assert np.isin(gpu["status"].cpu().numpy(), [cwc.CWC_TRAJ_DONE, cwc.CWC_TRAJ_STALLED]).all()
     # exact on-line moments == reduction of the dump (every trajectory)
     _assert_moments_equal_dump(gpu, P, cfg["n_replicas"])
     # sampled trajectories vs the oracle (first, last, ragged stride)
