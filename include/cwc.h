@@ -240,6 +240,18 @@ cwc_status cwc_stats_finalize(const cwc_stats *stats, int64_t n_cells, double *m
 cwc_status cwc_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count,
                              uint32_t *out, void *cuda_stream);
 
+/* Device draws (E = -log u1, u2) of Philox blocks (seed, g[i], n[i]) exactly
+ * as the SSA kernels form them (reading 3): E[i], u2[i]
+ * (device double arrays).  Test hook for the kernels' branch-free log. */
+cwc_status cwc_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
+                     void *cuda_stream);
+
+/* q[i] = e[i] / a[i] computed the way the SSA kernels compute tau = E / a0
+ * (P:206-207): the branch-free fast division where its range guard holds,
+ * IEEE div.rn otherwise.  Must equal the IEEE quotient bit for bit.  Device
+ * arrays.  Test hook. */
+cwc_status cwc_tau_div(const double *e, const double *a, int64_t count, double *q, void *cuda_stream);
+
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char *cwc_last_error(void);
 

@@ -55,9 +55,11 @@ struct cwc_model_s {
     std::vector<int32_t> re_ptr, re_cell, re_mult;
     std::vector<int32_t> nu_ptr, nu_cell, nu_delta;
     std::vector<int32_t> dep_ptr, dep;
+    std::vector<int2> dep_slot;   // warp path: (m, slot | owner << 24) per dependency entry
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
     int max_deps = 0;
+    int vbits = 31;   // observables are < 2^vbits (sums of int32 counts)
     bool thread_ok = false;
     ThreadTables tt{};
     // device copies (one allocation)
@@ -210,17 +212,28 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
     if (m->n_obs > 0) m->obs_of_cell.assign(d->obs_of_cell, d->obs_of_cell + ncell);
     else m->obs_of_cell.assign(ncell, -1);
     m->obs_ptr.assign(m->n_obs + 1, 0);
+    int max_obs_cells = 1;
     for (int o = 0; o < m->n_obs; ++o) {
         for (int c = 0; c < ncell; ++c)
             if (m->obs_of_cell[c] == o) m->obs_cells.push_back(c);
         m->obs_ptr[o + 1] = (int32_t)m->obs_cells.size();
+        max_obs_cells = std::max(max_obs_cells, m->obs_ptr[o + 1] - m->obs_ptr[o]);
     }
+    m->vbits = 31;
+    while ((1ll << (m->vbits - 31)) < max_obs_cells) ++m->vbits;
 
     // warp path sizes (pointers are filled by upload)
     m->wt.n_cells = m->n_cells;
     m->wt.M = m->M;
     m->wt.O = m->n_obs;
     m->wt.B = std::max(1, (m->M + 31) / 32);
+    m->wt.Bp = m->wt.B | 1;
+    if ((long long)32 * m->wt.Bp >= (1ll << 24)) return fail(CWC_ERR_UNSUPPORTED, "too many reactions for the warp path");
+    m->dep_slot.resize(m->dep.size());
+    for (size_t q = 0; q < m->dep.size(); ++q) {
+        const int r = m->dep[q], l = r / m->wt.B, k = r - l * m->wt.B;
+        m->dep_slot[q] = make_int2(r, (l * m->wt.Bp + k) | (l << 24));
+    }
 
     // thread path tables
     bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
@@ -272,7 +285,7 @@ cwc_status upload(cwc_model_s *m) {
     std::vector<int2> nu2(m->nu_cell.size());
     for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
     const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
-                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep), o_op = push_bytes(blob, m->obs_ptr),
+                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_op = push_bytes(blob, m->obs_ptr),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
     cudaError_t e = cudaGetDevice(&m->device);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaGetDevice");
@@ -287,7 +300,7 @@ cwc_status upload(cwc_model_s *m) {
     w.nu_ptr = (const int32_t *)(b + o_nup);
     w.nu = (const int2 *)(b + o_nu);
     w.dep_ptr = (const int32_t *)(b + o_dp);
-    w.dep = (const int32_t *)(b + o_dep);
+    w.dep = (const int2 *)(b + o_dep);
     w.obs_ptr = (const int32_t *)(b + o_op);
     w.obs_cells = (const int32_t *)(b + o_oc);
     w.init = (const int32_t *)(b + o_init);
@@ -308,6 +321,7 @@ struct Plan {
     int blocks = 0;
     // stats
     int stats_smem = 0;
+    StatLayout st{};
     int64_t cells_per_part = 0;
     int n_parts = 1;
     int64_t traj_per_part = 0;
@@ -391,38 +405,43 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             if (np_max >= pl.P) break;
         }
         const int64_t cells = stat_cells_round(np_max * J1 * O);
-        const size_t smem = (size_t)stat_bytes(cells);
+        const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
+        const size_t smem = (size_t)stat_bytes(lay_s, cells);
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
         bool use_smem = smem <= smem_cap && (int64_t)smem * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
         if (O == 0) use_smem = false;
         if (use_smem) {
             pl.stats_smem = 1;
+            pl.st = lay_s;
             pl.cells_per_part = std::max<int64_t>(cells, 4);
             pl.n_parts = pl.blocks;
             pl.traj_per_part = T;
             pl.smem_bytes = smem;
         } else {
             pl.stats_smem = 0;
+            pl.st = lay_g;
             pl.cells_per_part = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
             const int64_t budget = (int64_t)256 << 20;
-            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / stat_bytes(pl.cells_per_part)));
+            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / stat_bytes(pl.st, pl.cells_per_part)));
             pl.n_parts = (int)np;
             pl.traj_per_part = 0;
             pl.smem_bytes = 0;
         }
     } else {
         const WarpTables &w = m->wt;
-        int W = bt ? bt / 32 : 4;
+        int W = bt ? std::min(bt / 32, 4) : 4;  // ssa_warp_kernel is built for <= 128 threads
         if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
         pl.warps_per_block = W;
         const size_t per_warp = warp_smem_per_warp(w);
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
-        const size_t stats = (size_t)stat_bytes(cells);
+        const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
+        const size_t stats = (size_t)stat_bytes(lay_s, cells);
         bool use_smem = stats + W * per_warp <= 96 * 1024;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
         if (O == 0) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
+        pl.st = use_smem ? lay_s : lay_g;
         pl.cells_per_part = cells;
         pl.smem_bytes = (use_smem ? stats : 0) + W * per_warp;
         if (pl.smem_bytes > smem_cap + 27 * 1024) return fail(CWC_ERR_UNSUPPORTED, "warp path: per-warp state does not fit in shared memory");
@@ -437,12 +456,20 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         blocks = std::min<int64_t>(blocks, (pl.G + W - 1) / W);
         pl.blocks = (int)std::max<int64_t>(1, blocks);
         pl.threads = W * 32;
+        // a shared-memory part takes <= 2^16 trajectories (16-bit limbs); the
+        // kernel caps each CTA at that, so the grid must cover G with it
+        if (use_smem && (int64_t)pl.blocks * kSmemPartMaxTraj < pl.G) {
+            use_smem = false;
+            pl.stats_smem = 0;
+            pl.st = lay_g;
+            pl.smem_bytes = W * per_warp;
+        }
         pl.traj_per_part = 0;
         if (use_smem) {
             pl.n_parts = pl.blocks;
         } else {
             const int64_t budget = (int64_t)512 << 20;
-            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / stat_bytes(cells)));
+            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / stat_bytes(pl.st, cells)));
         }
     }
 
@@ -451,7 +478,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     pl.off_rates = off;
     off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
     pl.off_parts = off;
-    off = align256(off + (size_t)stat_bytes(pl.cells_per_part) * pl.n_parts);
+    off = align256(off + (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts);
     pl.off_trace = off;
     off = align256(off + sizeof(int64_t) * (size_t)std::max(opts ? opts->n_trace : 0, 1));
     pl.off_counter = off;
@@ -505,6 +532,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.rates = (const double *)(w + pl.off_rates);
     rp.parts = w + pl.off_parts;
     rp.cells_per_part = pl.cells_per_part;
+    rp.st = pl.st;
     rp.stats_smem = pl.stats_smem;
     rp.n_parts = pl.n_parts;
     rp.traj_per_part = pl.traj_per_part;
@@ -534,7 +562,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         }
     }
     if (!pl.stats_smem) {
-        e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)stat_bytes(pl.cells_per_part) * pl.n_parts, stream);
+        e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: zero partials");
     }
     e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);
@@ -678,6 +706,21 @@ cwc_status cwc_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, 
     if (count < 0 || (count > 0 && (!g || !n || !out))) return fail(CWC_ERR_INVALID, "bad arguments");
     cudaError_t e = launch_philox_blocks(seed, g, n, count, out, (cudaStream_t)cuda_stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_philox_blocks");
+    return CWC_OK;
+}
+
+cwc_status cwc_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
+                     void *cuda_stream) {
+    if (count < 0 || (count > 0 && (!g || !n || !E || !u2))) return fail(CWC_ERR_INVALID, "bad arguments");
+    cudaError_t e = launch_draws(seed, g, n, count, E, u2, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_draws");
+    return CWC_OK;
+}
+
+cwc_status cwc_tau_div(const double *num, const double *den, int64_t count, double *q, void *cuda_stream) {
+    if (count < 0 || (count > 0 && (!num || !den || !q))) return fail(CWC_ERR_INVALID, "bad arguments");
+    cudaError_t e = launch_tau_div(num, den, count, q, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_tau_div");
     return CWC_OK;
 }
 

@@ -24,11 +24,37 @@ struct ReactionDesc {
     int32_t rule;
 };
 
-// Statistics accumulator layout (device_common.cuh): kStatWords u32 word
-// arrays of n cells each (n a multiple of 4 so every part is 16-byte sized).
-constexpr int kStatWords = 7;
-__host__ __device__ __forceinline__ long long stat_bytes(long long n) { return 4ll * kStatWords * n; }
+// Statistics accumulator layout (device_common.cuh "limb accumulators").  A
+// part holds, per cell, one count word, sl limb words of the sum and ql limb
+// words of the sum of squares, as word arrays of n cells each (n a multiple
+// of 4 so every part is 16-byte sized).  Shared-memory parts use 32-bit words
+// with 16-bit limbs (<= 2^16 adds per word: one CTA); global parts use 64-bit
+// words with 32-bit limbs (<= 2^32 adds per word).  Limb adds never carry, so
+// every update is a fire-and-forget atomic (RED), never a dependent
+// read-modify-write chain.
+struct StatLayout {
+    int32_t wb;   // word bytes: 4 (16-bit limbs) or 8 (32-bit limbs)
+    int32_t sl;   // sum limbs
+    int32_t ql;   // sum-of-squares limbs
+    int32_t pad_;
+};
+__host__ __device__ __forceinline__ int stat_limb_bits(const StatLayout &l) { return l.wb == 4 ? 16 : 32; }
+__host__ __device__ __forceinline__ int stat_words(const StatLayout &l) { return 1 + l.sl + l.ql; }
+__host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, long long n) {
+    return (long long)l.wb * stat_words(l) * n;
+}
+constexpr long long kSmemPartMaxTraj = 1ll << 16;  // trajectories per shared-memory part (16-bit limbs)
 __host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }
+// Layout for observables of at most vbits bits (v < 2^vbits, v^2 < 2^(2 vbits)).
+__host__ __device__ __forceinline__ StatLayout stat_layout(bool smem, int vbits) {
+    StatLayout l;
+    l.wb = smem ? 4 : 8;
+    const int lb = smem ? 16 : 32;
+    l.sl = (vbits + lb - 1) / lb;
+    l.ql = (2 * vbits + lb - 1) / lb;
+    l.pad_ = 0;
+    return l;
+}
 
 // RNG key of local trajectory g: point * R_total + r_off + replica.
 __host__ __device__ __forceinline__ int64_t global_traj(int64_t g, int64_t R, int64_t R_total, int64_t r_off) {
@@ -48,7 +74,8 @@ struct RunParams {
     uint64_t seed;
     const double *rates;    // [P][M] flat per-reaction rate constants
     // statistics: accumulator parts (see stats.cu)
-    void *parts;            // n_parts x stat_bytes(cells_per_part)
+    void *parts;            // n_parts x stat_bytes(st, cells_per_part)
+    StatLayout st;          // word / limb layout of the parts (shared- or global-memory form)
     int64_t cells_per_part;
     int32_t stats_smem;     // 1: block accumulators in shared memory, flushed to parts[blockIdx]
     int32_t part_stride_blocks;  // GLOBAL mode: block b accumulates into part (b % n_parts)
@@ -79,13 +106,18 @@ struct ThreadTables {
 };
 
 // Warp path tables (device pointers, read through L1).
+// Reaction m lives in lane chunk l = m / B at position k = m % B; its
+// propensity is stored at shared-memory slot l * Bp + k (Bp = B | 1: odd, so a
+// lane-strided access and a chunk-contiguous access are both bank-conflict
+// free).
 struct WarpTables {
     int32_t n_cells, M, O, B;     // B = reactions per lane chunk = ceil(M / 32)
+    int32_t Bp, pad_[3];          // chunk stride (odd)
     const ReactionDesc *rx;       // [M]
     const int32_t *nu_ptr;        // [M+1]
     const int2 *nu;               // (cell, delta)
     const int32_t *dep_ptr;       // [M+1]
-    const int32_t *dep;
+    const int2 *dep;              // (m, slot | owner lane << 24) of every m in D(mu)
     const int32_t *obs_ptr;       // [O+1]
     const int32_t *obs_cells;
     const int32_t *init;          // [n_cells]
@@ -108,5 +140,8 @@ cudaError_t launch_stats_finalize(const int64_t *count, const int64_t *sum, cons
                                   double *mean, double *var, double *ci90, cudaStream_t stream);
 cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, uint32_t *out,
                                  cudaStream_t stream);
+cudaError_t launch_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
+                         cudaStream_t stream);
+cudaError_t launch_tau_div(const double *e, const double *a, int64_t count, double *q, cudaStream_t stream);
 
 }  // namespace cwc

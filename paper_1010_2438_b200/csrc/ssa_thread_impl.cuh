@@ -7,15 +7,34 @@
 //
 //   a_m   = k_m * double(h_m(x))                 Match, all M, registers
 //   cum_m = cum_{m-1} + a_m, a0 = cum_{M-1}      left-to-right, as the oracle
-//   tau   = E_n / a0, E_n = -log u1              P:206-207 (E_{n+1} precomputed:
-//                                                counter-based RNG is state-free)
+//   tau   = E_n / a0, E_n = -log u1
 //   samples j with j*dt <= t + tau get x (pre-event), on-line into the
 //   block's shared-memory moment accumulators (schema iii)
 //   mu    = #{m : cum_m <= u2 a0}                P:208-209 (cum is monotone)
 //   x    += nu_mu                                Update
 //
-// The cells and reactions are compile-time padded (S, M) so that x[] and
-// the propensities stay in registers; reaction tables are kernel parameters
+// Latency structure.  C1/C2 have fewer warps than the chip has schedulers,
+// so a firing costs the latency of its dependent chain, not its issue slots.
+// Only the state chain (x -> a -> a0 -> select -> x, and t += tau) is truly
+// serial; the Philox block and -log u1 of every future firing are state-free
+// (counter-based RNG).  The loop therefore runs in batches of B firings:
+//   * the draws of the NEXT batch (B independent Philox + log chains, each
+//     step B-wide, DrawPipe) are computed in four phases placed between the B
+//     firings of this batch -- one straight-line block with no branches
+//     (branch-free log and division), so the scheduler interleaves them;
+//   * the B firings run speculatively: each step applies its update at once
+//     (so the serial chain is only x -> a -> a0 -> select -> x) and records
+//     whether it was "plain": no sample crossed (t + tau < t_next), a0 in the
+//     fast-division range, no int32 overflow;
+//   * after the batch, a lane whose batch held a non-plain firing rolls back
+//     to the state before the first one and runs ONE exact iteration -- the
+//     oracle's loop body verbatim (crossing records, stall, end, overflow,
+//     IEEE division) -- then shifts its unused draws into place.
+// The committed sequence of firings is therefore exactly the sequential
+// algorithm's; batching only reorders independent RNG work.
+//
+// The cells and reactions are compile-time padded (S, M) so that x[] and the
+// propensities stay in registers; reaction tables are kernel parameters
 // (uniform constant-bank operands).  Net changes are packed int8 per cell
 // and selected branch-free while scanning the cumulative sums.
 #pragma once
@@ -34,8 +53,66 @@ __device__ __forceinline__ int pick(const int (&x)[S], int idx) {
     return v;
 }
 
+// cum_m = sum_{i<=m} a_i, left to right (== the oracle's a0 order).
+template <int S, int M>
+__device__ __forceinline__ void cumulative(const ThreadTables &tt, const int (&x)[S], const double (&c)[M],
+                                           double (&cum)[M]) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double a = __dmul_rn(c[m], combos(pick(x, tt.ia[m]), pick(x, tt.ib[m]), tt.sub[m], tt.shr[m]));
+        cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
+    }
+}
+
+// Packed net change of mu = #{m < M-1 : cum_m <= target} (first m with
+// target < cum_m; padded reactions have a_m = 0 and never win).
+template <int M, bool WANT_MU>
+__device__ __forceinline__ unsigned long long select_nu(const ThreadTables &tt, const double (&cum)[M], double target,
+                                                        int &mu) {
+    unsigned long long nu = tt.nu_pack[0];
+    int k = 0;
+#pragma unroll
+    for (int m = 0; m + 1 < M; ++m) {
+        const bool past = cum[m] <= target;
+        nu = past ? tt.nu_pack[m + 1] : nu;
+        if (WANT_MU) k += past ? 1 : 0;
+    }
+    mu = k;
+    return nu;
+}
+
+template <int S>
+__device__ __forceinline__ bool apply_nu(const int (&x)[S], unsigned long long nu, int (&xn)[S]) {
+    bool wrapped = false;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        xn[s] = x[s] + (int)(signed char)(unsigned char)(nu >> (8 * s));
+        wrapped |= (xn[s] < 0);  // counts are < 2^31 and |delta| <= 127: wrap <=> left int32
+    }
+    return wrapped;
+}
+
+template <int S>
+__device__ __forceinline__ void record_sample(const RunParams &rp, const ThreadTables &tt, const StatAcc &acc,
+                                              const int (&x)[S], long long cell_base, long long g, long long j) {
+    const int O = tt.O;
+    for (int o = 0; o < O; ++o) {
+        long long v = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)x[s] : 0ll;
+        stat_record(acc, cell_base + j * O + o, v);
+        if (rp.out_traj) rp.out_traj[(g * (long long)(rp.J + 1) + j) * O + o] = v;
+    }
+}
+
+template <int M>
+struct ThreadBatch {
+    static constexpr int B = (M <= 8) ? 4 : (M <= 16 ? 2 : 1);
+};
+
 template <int S, int M, bool TRACE>
 __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
+    constexpr int B = ThreadBatch<M>::B;
     extern __shared__ __align__(16) unsigned char smem[];
     const long long T = blockDim.x;
     const long long g0 = (long long)blockIdx.x * T;
@@ -47,15 +124,15 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
     StatAcc acc;
     long long p_base = 0;
     if (rp.stats_smem) {
-        acc = stat_view(smem, rp.cells_per_part);
+        acc = stat_view(smem, rp.cells_per_part, rp.st);
         uint4 *z = (uint4 *)smem;
-        const long long n16 = stat_bytes(rp.cells_per_part) / 16;
+        const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
         for (long long i = threadIdx.x; i < n16; i += T) z[i] = make_uint4(0, 0, 0, 0);
         p_base = g0 / rp.R;
         __syncthreads();
     } else {
-        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.cells_per_part),
-                        rp.cells_per_part);
+        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
+                        rp.cells_per_part, rp.st);
     }
 
     // Lanes past the last trajectory stay in the warp-uniform loop as idle
@@ -74,6 +151,12 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
                 if (rp.trace_g[i] == g) tslot = i;
             if (tslot >= 0) trace = rp.trace_buf + (long long)tslot * rp.trace_cap * 5;
         }
+        auto trace_rec = [&](unsigned long long n_, double a0, double tau, double tn, int mu) {
+            if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
+                double *r = trace + 5 * tn_rec++;
+                r[0] = (double)n_; r[1] = a0; r[2] = tau; r[3] = tn; r[4] = (double)mu;
+            }
+        };
 
         int x[S];
 #pragma unroll
@@ -82,100 +165,150 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
 #pragma unroll
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
 
-        auto record = [&](long long j) {
-            for (int o = 0; o < O; ++o) {
-                long long v = 0;
-#pragma unroll
-                for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)x[s] : 0ll;
-                stat_record(acc, cell_base + j * O + o, v);
-                if (rp.out_traj) rp.out_traj[(g * J1 + j) * O + o] = v;
-            }
-        };
-        auto trace_rec = [&](unsigned long long n, double a0, double tau, double tn, int mu) {
-            if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
-                double *r = trace + 5 * tn_rec++;
-                r[0] = (double)n; r[1] = a0; r[2] = tau; r[3] = tn; r[4] = (double)mu;
-            }
-        };
-
-        double t = 0.0, t_next = 0.0;
+        double t = 0.0, t_next = 0.0;  // t_next = j * dt: sample 0 is crossed by the first firing
         long long j = 0, firings = 0;
         unsigned long long n = 0;
         int status = 0;
-        double E, u2;
-        block_to_draws(philox_block(rp.seed, gk, 0), E, u2);
+        double Eb[B], Ub[B];
+#pragma unroll
+        for (int i = 0; i < B; ++i) block_to_draws(philox_block(rp.seed, gk, n + i), Eb[i], Ub[i]);
 
-        // Warp-uniform loop: every iteration reconverges at the vote, so the
-        // lanes of a warp advance their trajectories in lock-step and a lane
-        // that takes the rare path (crossing / end / stall) costs the others
-        // one short wait instead of splitting the warp for good.
         bool live = in_range;
         while (__any_sync(0xffffffffu, live)) {
-            if (!live) continue;
-            double cum[M];
+            // ---- fast batch: B firings run speculatively (every step commits
+            // its update); the four phases of the next batch's draws
+            // (n0+B .. n0+2B-1, valid if all B firings turn out plain) are
+            // interleaved with the steps so that the scheduler can overlap
+            // their independent chains with the serial state chain ----
+            const unsigned long long n0 = n;
+            double En[B], Un[B];
+            DrawPipe<B> pipe;
+            pipe.start(gk, n0 + B);
+            int xsnap[B][S];
+            double tsnap[B];
+            unsigned bad = 0;  // bit k: firing k of the batch is not plain
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
-                const double a = __dmul_rn(c[m], combos(pick(x, tt.ia[m]), pick(x, tt.ib[m]), tt.sub[m], tt.shr[m]));
-                cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
+            for (int k = 0; k < B; ++k) {
+#pragma unroll
+                for (int ph = 0; ph < 4; ++ph)
+                    if ((ph * B) / 4 == k) pipe.phase(ph, rp.seed, En, Un);
+#pragma unroll
+                for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
+                tsnap[k] = t;
+                double cum[M];
+                cumulative(tt, x, c, cum);
+                const double a0 = cum[M - 1];
+                const double tn = __dadd_rn(t, div_fast(Eb[k], a0));
+                int mu;
+                const unsigned long long nu = select_nu<M, false>(tt, cum, __dmul_rn(Ub[k], a0), mu);
+                int xn[S];
+                const bool wrapped = apply_nu(x, nu, xn);
+                // plain: fast division valid (a0 > 0 and in range), no sample
+                // crossed, no count left int32.  TRACE builds take every firing
+                // through the exact path below (it writes the trace).
+                const bool ok = !TRACE && div_fast_ok(Eb[k], a0) && (tn < t_next) && !wrapped;
+                bad |= ok ? 0u : (1u << k);
+#pragma unroll
+                for (int s = 0; s < S; ++s) x[s] = xn[s];
+                t = tn;
             }
-            const double a0 = cum[M - 1];
-            const double tau = __ddiv_rn(E, a0);
-            const double tn = __dadd_rn(t, tau);
-            const double target = __dmul_rn(u2, a0);
-            // next iteration's draw does not depend on the state: overlap it
-            double E1, u21;
-            block_to_draws(philox_block(rp.seed, gk, n + 1), E1, u21);
+            if (!live) bad = 1u;
+            const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
+            if (live) {
+                n += (unsigned long long)used;
+                firings += used;
+            }
 
-            bool apply = true;
-            if (!(tn < t_next)) {  // rare: sample crossing, end of horizon, or stall
-                if (a0 == 0.0) {
-                    for (; j <= J; ++j) record(j);
-                    status = CWC_TRAJ_STALLED;
-                    live = apply = false;
-                } else {
-                    while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
-                        record(j);
-                        ++j;
+            // ---- rare: roll back to the first non-plain firing, run ONE exact
+            // iteration (the oracle's loop body) and shift the draws ----
+            if (__any_sync(0xffffffffu, bad != 0u)) {
+                double E = Eb[0], u2 = Ub[0];  // draw of firing n (= batch slot `used`)
+                if (bad != 0u) {
+#pragma unroll
+                    for (int k = 0; k < B; ++k) {
+                        if (k == used) {
+#pragma unroll
+                            for (int s = 0; s < S; ++s) x[s] = xsnap[k][s];
+                            t = tsnap[k];
+                            E = Eb[k];
+                            u2 = Ub[k];
+                        }
                     }
-                    if (j > J) {
-                        trace_rec(n, a0, tau, tn, -1);
-                        status = CWC_TRAJ_DONE;
-                        live = apply = false;
+                }
+                if (live && bad != 0u) {
+                    double cum[M];
+                    cumulative(tt, x, c, cum);
+                    const double a0 = cum[M - 1];
+                    if (a0 == 0.0) {  // stall: no draw is consumed
+                        for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
+                        status = CWC_TRAJ_STALLED;
+                        live = false;
                     } else {
-                        t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                        const double tau = __ddiv_rn(E, a0);
+                        const double tn = __dadd_rn(t, tau);
+                        while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                            record_sample(rp, tt, acc, x, cell_base, g, j);
+                            ++j;
+                        }
+                        if (j > J) {  // horizon reached: drawn, not applied
+                            trace_rec(n, a0, tau, tn, -1);
+                            status = CWC_TRAJ_DONE;
+                            live = false;
+                        } else {
+                            t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                            int mu;
+                            const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
+                            int xn[S];
+                            if (apply_nu(x, nu, xn)) {  // a count would leave int32: freeze + fill
+                                for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
+                                status = CWC_TRAJ_OVERFLOW;
+                                live = false;
+                            } else {
+                                trace_rec(n, a0, tau, tn, mu);
+#pragma unroll
+                                for (int s = 0; s < S; ++s) x[s] = xn[s];
+                                t = tn;
+                                ++n;
+                                ++firings;
+                            }
+                        }
+                    }
+                    if (live) {
+                        // draws of firings n .. n+B-1 are slots [u, u+B) of
+                        // (this batch ++ next batch), u = n - n0 in [1, B]
+                        const int u = (int)(n - n0);
+                        double E2[B], U2[B];
+#pragma unroll
+                        for (int i = 0; i < B; ++i) {
+                            E2[i] = En[i];
+                            U2[i] = Un[i];
+#pragma unroll
+                            for (int cc = 1; cc < B; ++cc) {
+                                const int src = cc + i;
+                                if (cc == u) {
+                                    E2[i] = src < B ? Eb[src] : En[src - B];
+                                    U2[i] = src < B ? Ub[src] : Un[src - B];
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < B; ++i) {
+                            En[i] = E2[i];
+                            Un[i] = U2[i];
+                        }
                     }
                 }
             }
-            if (apply) {
-                unsigned long long nu = tt.nu_pack[0];
 #pragma unroll
-                for (int m = 0; m + 1 < M; ++m) nu = (cum[m] <= target) ? tt.nu_pack[m + 1] : nu;
-                if (TRACE && tslot >= 0) {
-                    int mu = 0;
-#pragma unroll
-                    for (int m = 0; m + 1 < M; ++m) mu += (cum[m] <= target) ? 1 : 0;
-                    trace_rec(n, a0, tau, tn, mu);
-                }
-                bool wrapped = false;
-#pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    x[s] += (int)(signed char)(unsigned char)(nu >> (8 * s));
-                    wrapped |= (x[s] < 0);
-                }
-                if (wrapped) {  // a count left int32: undo, freeze, fill
-#pragma unroll
-                    for (int s = 0; s < S; ++s) x[s] -= (int)(signed char)(unsigned char)(nu >> (8 * s));
-                    for (; j <= J; ++j) record(j);
-                    status = CWC_TRAJ_OVERFLOW;
-                    live = false;
-                } else {
-                    t = tn;
-                    ++firings;
-                    ++n;
-                    E = E1;
-                    u2 = u21;
-                }
+            for (int i = 0; i < B; ++i) {
+                Eb[i] = En[i];
+                Ub[i] = Un[i];
             }
+            // reconverge the warp explicitly: the vote at the loop head only
+            // synchronises it, and a warp left split after the rare path would
+            // run every later batch twice with half its lanes (a plain
+            // __syncwarp() is elided by the compiler here)
+            asm volatile("bar.warp.sync -1;" ::: "memory");
         }
         if (in_range) {
             if (rp.out_firings) rp.out_firings[g] = firings;
@@ -186,8 +319,8 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
 
     if (rp.stats_smem) {  // coalesced, vectorised flush of the block's partial moments
         __syncthreads();
-        const long long n16 = stat_bytes(rp.cells_per_part) / 16;
-        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.cells_per_part));
+        const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.st, rp.cells_per_part));
         const uint4 *src = (const uint4 *)smem;
         for (long long i = threadIdx.x; i < n16; i += T) dst[i] = src[i];
     }
@@ -195,7 +328,7 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
 
 template <int S, int M>
 cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, size_t smem, cudaStream_t st,
-                             bool trace) {
+                      bool trace) {
     const long long blocks = (rp.G + threads - 1) / threads;
     if (trace) {
         auto k = ssa_thread_kernel<S, M, true>;
@@ -213,7 +346,7 @@ cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, 
 
 template <int S>
 cudaError_t launch_s(int m_pad, const RunParams &rp, const ThreadTables &tt, int threads, size_t smem,
-                            cudaStream_t st, bool trace) {
+                     cudaStream_t st, bool trace) {
     switch (m_pad) {
         case 2: return launch_sm<S, 2>(rp, tt, threads, smem, st, trace);
         case 3: return launch_sm<S, 3>(rp, tt, threads, smem, st, trace);

@@ -9,19 +9,23 @@
 // atomic counter (schema i, on-demand dispatch).
 //
 // Per warp, in shared memory: counts x[cell] (int32, plus a constant 1 at
-// index n_cells for absent reactants) and propensities a[m] in a
-// lane-chunked layout: lane l owns reactions m in [l*B, (l+1)*B), stored at
-// a[k*32 + l] (bank-conflict free).  Lane l keeps its chunk sum in a
-// register; a Kogge-Stone shuffle scan over the 32 chunk sums gives the
-// inclusive prefixes, a0 = prefix of lane 31.
+// index n_cells for absent reactants) and propensities a[m].  Lane l owns the
+// chunk of reactions m in [l*B, (l+1)*B), stored contiguously at slots
+// l*Bp .. l*Bp+B-1 (Bp = B | 1, odd: the lane-strided re-sum and the
+// chunk-contiguous selection read are both bank-conflict free).  Lane l keeps
+// its chunk sum (left to right) in a register; a Kogge-Stone shuffle scan of
+// the 32 chunk sums gives the inclusive prefixes, a0 = prefix of lane 31
+// (P:201-203).
 //
 // One firing (Fig. fig:simd P:608-621):
 //   tau = E_n / a0 (E_n = -log u1 of Philox block n, drawn 32 at a time: lane
 //   i computes block n_base + i, then broadcast by shuffle), sample crossing
-//   into the block's moment accumulators, target = u2 a0,
-//   L = ffs(ballot(prefix_l > target)), lane L scans its chunk from the
-//   exclusive prefix, x += nu_mu (one lane per changed cell), then only the
-//   reactions in D(mu) are recomputed and only their owner lanes re-sum.
+//   into the moment accumulators, target = u2 a0,
+//   L = ffs(ballot(prefix_l > target)) picks the chunk; the lanes then read
+//   chunk L (lane k <- a[L*Bp + k]), shuffle-scan it from L's exclusive
+//   prefix and ffs(ballot(prefix > target)) picks mu inside it; x += nu_mu
+//   (one lane per changed cell); only the reactions in D(mu) are recomputed
+//   (precomputed slots) and only their owner lanes re-sum their chunks.
 #include <cuda_runtime.h>
 
 #include "cwc_internal.h"
@@ -38,7 +42,7 @@ __device__ __forceinline__ double propensity(const WarpTables &wt, const int *xs
     return __dmul_rn(__ldg(rates + m), combos(xs[d.x], xs[d.y], d.z & 1, d.z >> 1));
 }
 
-// Inclusive Kogge-Stone scan of the 32 chunk sums.
+// Inclusive Kogge-Stone scan over the 32 lanes.
 __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -48,44 +52,64 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-__global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
+template <bool TRACE>
+__global__ void __launch_bounds__(128, 6) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
                                                        int per_warp_bytes, int x_bytes) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
-    const int B = wt.B;
+    const int B = wt.B, Bp = wt.Bp;
     const int O = wt.O;
     const int M = wt.M;
     const long long J = rp.J, J1 = J + 1;
 
     StatAcc acc;
     if (rp.stats_smem) {
-        acc = stat_view(smem, rp.cells_per_part);
+        acc = stat_view(smem, rp.cells_per_part, rp.st);
         uint4 *z = (uint4 *)smem;
         for (long long i = threadIdx.x; i < stats_smem_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
     } else {
-        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.cells_per_part),
-                        rp.cells_per_part);
+        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
+                        rp.cells_per_part, rp.st);
     }
     int *xs = (int *)(smem + stats_smem_bytes + (long long)wib * per_warp_bytes);
     double *as = (double *)((unsigned char *)xs + x_bytes);
+    __shared__ unsigned int cta_traj;  // trajectories taken by this CTA (shared-memory part capacity)
+    if (threadIdx.x == 0) cta_traj = 0;
     __syncthreads();
 
     for (;;) {
-        unsigned long long gg = 0;
-        if (lane == 0) gg = atomicAdd(rp.next_traj, 1ull);
-        const long long g = (long long)__shfl_sync(kFull, gg, 0);
-        if (g >= rp.G) break;
+        unsigned long long gg = ~0ull;
+        if (lane == 0) {
+            // a shared-memory part holds <= kSmemPartMaxTraj trajectories (16-bit
+            // limbs); the host sizes the grid so that the capped CTAs cover G
+            if (!rp.stats_smem || atomicAdd(&cta_traj, 1u) < (unsigned)kSmemPartMaxTraj) gg = atomicAdd(rp.next_traj, 1ull);
+        }
+        gg = __shfl_sync(kFull, gg, 0);
+        if (gg >= (unsigned long long)rp.G) break;
+        const long long g = (long long)gg;
         const long long p = g / rp.R;
         const double *rates = rp.rates + p * M;
         const long long cell_base = p * J1 * O;
         const uint64_t gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);  // RNG stream id
 
         int tslot = -1;
-        for (int i = 0; i < rp.n_trace; ++i)
-            if (rp.trace_g[i] == g) tslot = i;
-        double *trace = (tslot >= 0) ? rp.trace_buf + (long long)tslot * rp.trace_cap * 5 : nullptr;
+        double *trace = nullptr;
         long long tn_rec = 0;
+        if (TRACE) {
+            for (int i = 0; i < rp.n_trace; ++i)
+                if (rp.trace_g[i] == g) tslot = i;
+            if (tslot >= 0) trace = rp.trace_buf + (long long)tslot * rp.trace_cap * 5;
+        }
+        auto trace_rec = [&](unsigned long long n_, double a0_, double tau, double tn, int mu) {
+            if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
+                if (lane == 0) {
+                    double *r = trace + 5 * tn_rec;
+                    r[0] = (double)n_; r[1] = a0_; r[2] = tau; r[3] = tn; r[4] = (double)mu;
+                }
+                ++tn_rec;
+            }
+        };
 
         for (int c = lane; c < wt.n_cells; c += 32) xs[c] = __ldg(wt.init + c);
         if (lane == 0) xs[wt.n_cells] = 1;
@@ -95,13 +119,14 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
         for (int k = 0; k < B; ++k) {
             const int m = lane * B + k;
             const double a = (m < M) ? propensity(wt, xs, rates, m) : 0.0;
-            as[k * 32 + lane] = a;
+            as[lane * Bp + k] = a;
             part = (k == 0) ? a : __dadd_rn(part, a);
         }
         double incl = warp_incl_scan(part, lane);
         double a0 = shfl_d(incl, 31);
         double excl = __shfl_up_sync(kFull, incl, 1);
         if (lane == 0) excl = 0.0;
+        __syncwarp();
 
         auto record = [&](long long j) {
             for (int o = lane; o < O; o += 32) {
@@ -110,13 +135,6 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
                 stat_record(acc, cell_base + j * O + o, v);
                 if (rp.out_traj) rp.out_traj[(g * J1 + j) * O + o] = v;
             }
-        };
-        auto trace_rec = [&](unsigned long long n, double a0_, double tau, double tn, int mu) {
-            if (tslot >= 0 && lane == 0 && tn_rec < rp.trace_cap) {
-                double *r = trace + 5 * tn_rec;
-                r[0] = (double)n; r[1] = a0_; r[2] = tau; r[3] = tn; r[4] = (double)mu;
-            }
-            if (tslot >= 0 && tn_rec < rp.trace_cap) ++tn_rec;
         };
 
         double t = 0.0, t_next = 0.0;
@@ -134,7 +152,8 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
             const int i = (int)(n - n_base);
             const double E = shfl_d(El, i);
             const double u2 = shfl_d(u2l, i);
-            const double tau = __ddiv_rn(E, a0);
+            // warp-uniform operands: the fast/IEEE choice never diverges
+            const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
             const double tn = __dadd_rn(t, tau);
             if (!(tn < t_next)) {
                 if (a0 == 0.0) {
@@ -154,22 +173,31 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
                 t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
             }
             const double target = __dmul_rn(u2, a0);
-            const unsigned mask = __ballot_sync(kFull, incl > target);
-            const int L = __ffs(mask) - 1;  // mask != 0: prefix of lane 31 is a0 > target
+            const int L = __ffs(__ballot_sync(kFull, incl > target)) - 1;  // lane 31's prefix is a0 > target
+            // inside chunk L: shuffle-scan its entries from L's exclusive prefix
+            double carry = shfl_d(excl, L);
             int mu = -1;
-            if (lane == L) {
-                double c = excl;
-                int last_pos = -1;
-                for (int k = 0; k < B; ++k) {
-                    const double a = as[k * 32 + L];
-                    c = __dadd_rn(c, a);
-                    if (a > 0.0) last_pos = k;
-                    if (target < c) { mu = L * B + k; break; }
+            unsigned pos_any = 0;
+            int pos_base = 0;
+            for (int k0 = 0; k0 < B; k0 += 32) {
+                const int k = k0 + lane;
+                const double a = (k < B) ? as[L * Bp + k] : 0.0;
+                const double c = __dadd_rn(carry, warp_incl_scan(a, lane));
+                const unsigned hit = __ballot_sync(kFull, k < B && target < c);
+                const unsigned pos = __ballot_sync(kFull, a > 0.0);
+                if (hit) {
+                    mu = L * B + k0 + __ffs(hit) - 1;
+                    break;
                 }
-                // the chunk's own left-to-right sum may round below the scanned prefix
-                if (mu < 0) mu = L * B + last_pos;
+                if (pos) {
+                    pos_any = pos;
+                    pos_base = k0;
+                }
+                carry = shfl_d(c, 31);
             }
-            mu = __shfl_sync(kFull, mu, L);
+            // the chunk's scanned sums may round below the lane prefix: take
+            // its last positive entry
+            if (mu < 0) mu = L * B + pos_base + 31 - __clz(pos_any);
             trace_rec(n, a0, tau, tn, mu);
 
             // Update: one lane per changed cell; distinct cells.
@@ -192,16 +220,16 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
             unsigned dirty = 0;
             const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
             for (int q = db + lane; q < de; q += 32) {
-                const int m = __ldg(wt.dep + q);
-                const int owner = m / B, k = m - owner * B;
-                as[k * 32 + owner] = propensity(wt, xs, rates, m);
-                dirty |= 1u << owner;
+                const int2 d = __ldg(wt.dep + q);
+                as[d.y & 0xffffff] = propensity(wt, xs, rates, d.x);
+                dirty |= 1u << (d.y >> 24);
             }
             dirty = __reduce_or_sync(kFull, dirty);
             __syncwarp();
             if ((dirty >> lane) & 1u) {
-                double s = as[lane];
-                for (int k = 1; k < B; ++k) s = __dadd_rn(s, as[k * 32 + lane]);
+                const double *ch = as + lane * Bp;
+                double s = ch[0];
+                for (int k = 1; k < B; ++k) s = __dadd_rn(s, ch[k]);
                 part = s;
             }
             incl = warp_incl_scan(part, lane);
@@ -212,19 +240,20 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
             t = tn;
             ++firings;
             ++n;
+            asm volatile("bar.warp.sync -1;" ::: "memory");  // keep the warp converged
         }
         if (lane == 0) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
-            if (tslot >= 0) rp.trace_len[tslot] = tn_rec;
+            if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
         }
         __syncwarp();
     }
 
     if (rp.stats_smem) {
         __syncthreads();
-        const long long n16 = stat_bytes(rp.cells_per_part) / 16;
-        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.cells_per_part));
+        const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.st, rp.cells_per_part));
         const uint4 *src = (const uint4 *)smem;
         for (long long q = threadIdx.x; q < n16; q += blockDim.x) dst[q] = src[q];
     }
@@ -233,17 +262,18 @@ __global__ void __launch_bounds__(256) ssa_warp_kernel(const RunParams rp, const
 static inline int align16(long long v) { return (int)((v + 15) & ~15ll); }
 
 size_t warp_smem_per_warp(const WarpTables &wt) {
-    return (size_t)align16(4ll * (wt.n_cells + 1)) + (size_t)8 * 32 * wt.B;
+    return (size_t)align16(4ll * (wt.n_cells + 1)) + (size_t)8 * 32 * wt.Bp;
 }
 
 cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                             size_t smem_bytes, cudaStream_t stream) {
-    const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.cells_per_part) : 0;
+    const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
     const int x_bytes = align16(4ll * (wt.n_cells + 1));
     const int per_warp = (int)warp_smem_per_warp(wt);
-    cudaError_t e = cudaFuncSetAttribute(ssa_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    auto k = (rp.n_trace > 0) ? ssa_warp_kernel<true> : ssa_warp_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
-    ssa_warp_kernel<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);
+    k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);
     return cudaGetLastError();
 }
 

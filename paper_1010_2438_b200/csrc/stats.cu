@@ -1,9 +1,10 @@
 // stats.cu -- second stage of the on-line reduction, finalize, Philox hook.
 //
 // Stage 1 (inside the SSA kernels) leaves one partial moment set per part
-// (per CTA, or per CTA slice): 7 little-endian u32 word arrays over the
-// part's cells (count; sum lo/hi; sumsq w0..w3).  Stage 2 sums, for every (point, sample, observable)
-// cell, the parts that cover its point and writes count / sum / sumsq(128)
+// (per CTA, or per CTA slice) in limb form (cwc_internal.h StatLayout: count
+// word, sum limbs, sum-of-squares limbs).  Stage 2 sums, for every (point,
+// sample, observable) cell, the parts that cover its point, recombines the
+// limbs and writes count / sum / sumsq(128)
 // -- exact integer addition, so the result does not depend on how
 // trajectories were spread over CTAs (SPEC S:513 determinism).
 #include <cuda_runtime.h>
@@ -16,6 +17,10 @@ namespace cwc {
 __global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n_cells, int64_t *count, int64_t *sum,
                                     uint64_t *sumsq) {
     const long long JO = (long long)(rp.J + 1) * O;
+    const StatLayout L = rp.st;
+    const int lb = stat_limb_bits(L);
+    const long long pb = stat_bytes(L, rp.cells_per_part);
+    const long long n = rp.cells_per_part;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n_cells;
          c += (long long)gridDim.x * blockDim.x) {
         const long long p = c / JO;
@@ -29,18 +34,27 @@ __global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n
             b0 = 0;
             b1 = rp.n_parts - 1;
         }
-        unsigned long long cnt = 0, s1 = 0;
-        unsigned __int128 s2 = 0;
+        // per-word totals over the parts (each word < 2^64 per part; at most
+        // 2^31 parts) accumulated in 128 bits, then limbs recombined
+        unsigned __int128 w[1 + 8 + 16];
+        const int nw = stat_words(L);
+        for (int k = 0; k < nw; ++k) w[k] = 0;
         for (long long b = b0; b <= b1; ++b) {
             long long local = c;
             if (rp.traj_per_part > 0) local = (p - (b * rp.traj_per_part) / rp.R) * JO + rest;
-            const StatAcc a = stat_view((unsigned char *)rp.parts + b * stat_bytes(rp.cells_per_part), rp.cells_per_part);
-            cnt += a.w[0][local];
-            s1 += (unsigned long long)a.w[1][local] | ((unsigned long long)a.w[2][local] << 32);
-            s2 += (unsigned __int128)((unsigned long long)a.w[3][local] | ((unsigned long long)a.w[4][local] << 32)) +
-                  ((unsigned __int128)((unsigned long long)a.w[5][local] | ((unsigned long long)a.w[6][local] << 32)) << 64);
+            const unsigned char *base = (const unsigned char *)rp.parts + b * pb;
+            if (L.wb == 4) {
+                const unsigned int *u = (const unsigned int *)base + local;
+                for (int k = 0; k < nw; ++k) w[k] += u[(long long)k * n];
+            } else {
+                const unsigned long long *u = (const unsigned long long *)base + local;
+                for (int k = 0; k < nw; ++k) w[k] += u[(long long)k * n];
+            }
         }
-        count[c] = (int64_t)cnt;
+        unsigned __int128 s1 = 0, s2 = 0;
+        for (int i = 0; i < L.sl; ++i) s1 += w[1 + i] << (lb * i);
+        for (int i = 0; i < L.ql; ++i) s2 += w[1 + L.sl + i] << (lb * i);
+        count[c] = (int64_t)w[0];
         sum[c] = (int64_t)s1;
         sumsq[2 * c] = (uint64_t)s2;
         sumsq[2 * c + 1] = (uint64_t)(s2 >> 64);
@@ -141,6 +155,41 @@ cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t 
     long long blocks = (count + 255) / 256;
     if (blocks > 148 * 32) blocks = 148 * 32;
     philox_blocks_kernel<<<(unsigned)blocks, 256, 0, stream>>>(seed, g, n, count, out);
+    return cudaGetLastError();
+}
+
+// ---- draw / division hooks (the SSA kernels' own device functions) ------------
+__global__ void draws_kernel(uint64_t seed, const int64_t *g, const int64_t *n, long long count, double *E,
+                             double *u2) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+        double e, u;
+        block_to_draws(philox_block(seed, (uint64_t)g[i], (uint64_t)n[i]), e, u);
+        E[i] = e;
+        u2[i] = u;
+    }
+}
+
+__global__ void tau_div_kernel(const double *e, const double *a, long long count, double *q) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+        const double x = e[i], y = a[i];
+        q[i] = div_fast_ok(x, y) ? div_fast(x, y) : __ddiv_rn(x, y);
+    }
+}
+
+cudaError_t launch_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
+                         cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    long long blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    draws_kernel<<<(unsigned)blocks, 256, 0, stream>>>(seed, g, n, count, E, u2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tau_div(const double *e, const double *a, int64_t count, double *q, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    long long blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    tau_div_kernel<<<(unsigned)blocks, 256, 0, stream>>>(e, a, count, q);
     return cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
 
 EXPORTED = ["cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
             "cwc_simulate_workspace_size", "cwc_simulate", "cwc_simulate_host", "cwc_simulate_host_workspace_size",
-            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_last_error"]
+            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_tau_div", "cwc_last_error"]
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32
@@ -88,6 +88,8 @@ def lib():
                                                        ctypes.POINTER(ctypes.c_size_t)]
         L.cwc_stats_finalize.argtypes = [ctypes.POINTER(cwc_stats), I64, P, P, P, P]
         L.cwc_philox_blocks.argtypes = [ctypes.c_uint64, P, P, I64, P, P]
+        L.cwc_draws.argtypes = [ctypes.c_uint64, P, P, I64, P, P, P]
+        L.cwc_tau_div.argtypes = [P, P, I64, P, P]
         L.cwc_last_error.restype = ctypes.c_char_p
         L.cwc_last_error.argtypes = []
         for name in EXPORTED:
@@ -248,6 +250,14 @@ def cwc_stats_finalize(stats, n_cells, mean, var, ci90, stream):
 
 def cwc_philox_blocks(seed, g, n, out, stream):
     _check(lib().cwc_philox_blocks(int(seed), _ptr(g), _ptr(n), int(g.numel()), _ptr(out), ctypes.c_void_p(stream)))
+
+
+def cwc_draws(seed, g, n, E, u2, stream):
+    _check(lib().cwc_draws(int(seed), _ptr(g), _ptr(n), int(g.numel()), _ptr(E), _ptr(u2), ctypes.c_void_p(stream)))
+
+
+def cwc_tau_div(e, a, q, stream):
+    _check(lib().cwc_tau_div(_ptr(e), _ptr(a), int(e.numel()), _ptr(q), ctypes.c_void_p(stream)))
 
 
 # ---------------------------------------------------------------------------

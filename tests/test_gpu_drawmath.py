@@ -1,0 +1,108 @@
+"""GPU: the SSA kernels' branch-free draw arithmetic (device_common.cuh).
+
+* tau = E / a0 must be the IEEE quotient bit for bit: the
+  kernels' fast division is checked against numpy's (IEEE) division over the
+  whole input range, fast-path range and edges included.
+* E = -log u1 comes from the kernels' own branch-free log: u2 must
+  equal the oracle's bit for bit; E must be within 1 ulp of the
+  correctly rounded value (mpmath, 200 bits) and equal to the oracle's
+  glibc log in all but a small fraction of draws (DESIGN.md "Parity":
+  a one-ulp E moves tau by one ulp, the traced "log-ulp" class).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_1010_2438_b200 import cwc  # noqa: E402
+
+
+def _ulps(a, b):
+    """|a - b| in ulps for finite doubles of equal sign (exact int64 arithmetic)."""
+    return np.abs(a.view(np.int64) - b.view(np.int64))
+
+
+def _tau_div(e, a):
+    et = torch.as_tensor(e, device="cuda")
+    at = torch.as_tensor(a, device="cuda")
+    q = torch.empty_like(et)
+    cwc.cwc_tau_div(et, at, q, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return q.cpu().numpy()
+
+
+def test_tau_division_is_ieee_fast_range():
+    rng = np.random.default_rng(11)
+    n = 1 << 22
+    u = (rng.integers(0, 1 << 53, size=n, dtype=np.int64) + 1).astype(np.float64) * 2.0**-53
+    e = -np.log(u)                                    # the E values the method produces
+    a = 10.0 ** rng.uniform(-12, 15, size=n)          # propensity sums of every config and beyond
+    q = _tau_div(e, a)
+    want = e / a
+    assert np.array_equal(q.view(np.int64), want.view(np.int64))
+
+
+def test_tau_division_is_ieee_edges():
+    rng = np.random.default_rng(12)
+    n = 1 << 20
+    e = np.concatenate([rng.uniform(0, 40, n // 2), 10.0 ** rng.uniform(-320, 300, n // 2)])
+    a = np.concatenate([10.0 ** rng.uniform(-320, 308, n // 2), rng.uniform(1e-3, 1e3, n // 2)])
+    edges_e = np.array([0.0, -0.0, 2.0**-60, 2.0**-61, 64.0, 64.0000001, 1.0, 36.7368005696771, 5e-324, np.inf])
+    edges_a = np.array([0.0, 1.0, 2.0**-900, 2.0**-901, 2.0**900, 2.0**901, 1e-310, 3.0, np.inf, np.nan])
+    E, A = np.meshgrid(edges_e, edges_a)
+    e = np.concatenate([e, E.ravel()])
+    a = np.concatenate([a, A.ravel()])
+    with np.errstate(all="ignore"):
+        want = e / a
+    q = _tau_div(e, a)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(q), nan)
+    assert np.array_equal(q[~nan].view(np.int64), want[~nan].view(np.int64))
+
+
+def test_draws_match_oracle_and_are_accurate():
+    rng = np.random.default_rng(13)
+    seed = 1
+    n_traj, per = 64, 4096
+    g = np.repeat(rng.integers(0, 1 << 40, size=n_traj, dtype=np.int64), per)
+    n0 = rng.integers(0, 1 << 30, size=n_traj, dtype=np.int64)
+    n = (np.repeat(n0, per) + np.tile(np.arange(per, dtype=np.int64), n_traj))
+    E = torch.empty(g.size, dtype=torch.float64, device="cuda")
+    U = torch.empty_like(E)
+    cwc.cwc_draws(seed, torch.as_tensor(g, device="cuda"), torch.as_tensor(n, device="cuda"), E, U,
+                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    E = E.cpu().numpy()
+    U = U.cpu().numpy()
+    oe, ou = [], []
+    for i in range(n_traj):
+        tau, u2 = oracle.tau_stream(seed, int(g[i * per]), int(n0[i]), per, 1.0)  # a0 = 1: tau == E exactly
+        oe.append(tau)
+        ou.append(u2)
+    oe = np.concatenate(oe)
+    ou = np.concatenate(ou)
+    assert np.array_equal(U.view(np.int64), ou.view(np.int64))
+    d = _ulps(E, oe)
+    assert d.max() <= 1
+    assert (d == 0).mean() >= 0.98, (d == 0).mean()
+    # accuracy against the correctly rounded value on a subsample
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.prec = 200
+    worst = 0.0
+    for i in rng.choice(E.size, size=3000, replace=False):
+        w = oracle.philox4x32_10([int(n[i]) & 0xFFFFFFFF, int(n[i]) >> 32, int(g[i]) & 0xFFFFFFFF, int(g[i]) >> 32],
+                                 [seed, 0])
+        u1, _ = oracle.uniforms(w)
+        if u1 == 1.0:
+            continue
+        ex = -mpmath.log(mpmath.mpf(u1))
+        ulp = mpmath.mpf(2) ** (mpmath.floor(mpmath.log(ex, 2)) - 52)
+        worst = max(worst, float(abs(mpmath.mpf(float(E[i])) - ex) / ulp))
+    assert worst < 1.0, worst

@@ -105,6 +105,11 @@ SMALL = [
     ("dimer", lambda: (w.dimerisation_model(50, 0.1), None), dict(t_end=3.0, sample_dt=0.1, n_replicas=129, seed=8)),
     ("paper", lambda: (w.paper_example_model(0.5), None), dict(t_end=5.0, sample_dt=0.5, n_replicas=40, seed=2)),
     ("one", lambda: (w.config("C1")[0], None), dict(t_end=3.0, sample_dt=3.0, n_replicas=1, seed=5)),
+    # thread-path batch widths 2 and 1 (M in 9..16 and 17..32), all 8 register cells
+    ("rnd12", lambda: (w.random_network_model(seed=3, n_species=6, n_reactions=12), None),
+     dict(t_end=0.5, sample_dt=0.05, n_replicas=70, seed=2)),
+    ("rnd24", lambda: (w.random_network_model(seed=5, n_species=8, n_reactions=24), None),
+     dict(t_end=0.2, sample_dt=0.02, n_replicas=45, seed=3)),
 ]
 
 
