@@ -321,6 +321,7 @@ struct Plan {
     int blocks = 0;
     // stats
     int stats_smem = 0;
+    int ws = 0;
     StatLayout st{};
     int64_t cells_per_part = 0;
     int n_parts = 1;
@@ -387,12 +388,18 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         pl.s_pad = thread_pad_cells(m->n_cells);
         pl.m_pad = thread_pad_reactions(std::max(m->M, 2));
         if (pl.s_pad < 0 || pl.m_pad < 0) return fail(CWC_ERR_INVALID, "thread path padding");
-        int T = bt;
-        if (!T) {
-            T = 32;
-            for (int cand : {64, 128, 256})
-                if ((pl.G + cand - 1) / cand >= 2ll * nsm) T = cand;
-        }
+        // one-warp CTAs: the block scheduler then spreads trajectories of
+        // unequal length (sweeps: 17x spread in C3) evenly over the SMs and
+        // refills SMs as warps finish; the thread path is latency-bound, so
+        // nothing is gained from larger CTAs
+        int T = bt ? bt : 32;
+        // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories)
+        // when the consumer warps alone leave sub-partitions idle
+        const bool tracing = opts && opts->n_trace > 0;
+        bool ws = !tracing && !bt && (pl.G + 31) / 32 <= 4ll * nsm;
+        if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
+        if (ws) T = 32;
+        pl.ws = ws ? 1 : 0;
         pl.threads = T;
         const int64_t blocks = (pl.G + T - 1) / T;
         if (blocks > 0x7fffffffll) return fail(CWC_ERR_INVALID, "too many trajectories for one launch");
@@ -407,8 +414,10 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int64_t cells = stat_cells_round(np_max * J1 * O);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t smem = (size_t)stat_bytes(lay_s, cells);
+        const size_t extra = ws ? kWsRingBytes : 0;
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
-        bool use_smem = smem <= smem_cap && (int64_t)smem * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
+        bool use_smem = smem + extra <= smem_cap &&
+                        (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
         if (O == 0) use_smem = false;
         if (use_smem) {
@@ -417,7 +426,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             pl.cells_per_part = std::max<int64_t>(cells, 4);
             pl.n_parts = pl.blocks;
             pl.traj_per_part = T;
-            pl.smem_bytes = smem;
+            pl.smem_bytes = smem + extra;
         } else {
             pl.stats_smem = 0;
             pl.st = lay_g;
@@ -426,7 +435,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / stat_bytes(pl.st, pl.cells_per_part)));
             pl.n_parts = (int)np;
             pl.traj_per_part = 0;
-            pl.smem_bytes = 0;
+            pl.smem_bytes = extra;
         }
     } else {
         const WarpTables &w = m->wt;
@@ -437,7 +446,10 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t stats = (size_t)stat_bytes(lay_s, cells);
-        bool use_smem = stats + W * per_warp <= 96 * 1024;
+        // shared-memory statistics only while they cost no occupancy (the
+        // kernel holds 8 CTAs of 4 warps per SM): crossings are rare, so the
+        // global-memory parts (fire-and-forget REDs to L2) are nearly free
+        bool use_smem = (stats + W * per_warp) * 8 <= 200 * 1024;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
         if (O == 0) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
@@ -533,6 +545,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.parts = w + pl.off_parts;
     rp.cells_per_part = pl.cells_per_part;
     rp.st = pl.st;
+    rp.ws = pl.ws;
     rp.stats_smem = pl.stats_smem;
     rp.n_parts = pl.n_parts;
     rp.traj_per_part = pl.traj_per_part;

@@ -43,6 +43,10 @@ __host__ __device__ __forceinline__ int stat_words(const StatLayout &l) { return
 __host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, long long n) {
     return (long long)l.wb * stat_words(l) * n;
 }
+// warp-specialised thread path (ssa_thread_ws.cuh): draws in flight per
+// trajectory and the ring + hand-off counters' shared-memory bytes per CTA
+constexpr int kWsRing = 32;
+constexpr size_t kWsRingBytes = (size_t)2 * kWsRing * 32 * sizeof(double) + 3 * 32 * sizeof(unsigned);
 constexpr long long kSmemPartMaxTraj = 1ll << 16;  // trajectories per shared-memory part (16-bit limbs)
 __host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }
 // Layout for observables of at most vbits bits (v < 2^vbits, v^2 < 2^(2 vbits)).
@@ -78,6 +82,7 @@ struct RunParams {
     StatLayout st;          // word / limb layout of the parts (shared- or global-memory form)
     int64_t cells_per_part;
     int32_t stats_smem;     // 1: block accumulators in shared memory, flushed to parts[blockIdx]
+    int32_t ws;             // thread path: warp-specialised producer/consumer kernel (ssa_thread_ws.cuh)
     int32_t part_stride_blocks;  // GLOBAL mode: block b accumulates into part (b % n_parts)
     int32_t n_parts;
     int64_t traj_per_part;  // static mapping: part b covers g in [b*T, (b+1)*T); 0 = all points

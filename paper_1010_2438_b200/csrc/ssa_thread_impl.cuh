@@ -327,9 +327,19 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
 }
 
 template <int S, int M>
+__global__ void ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt);
+
+template <int S, int M>
 cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, size_t smem, cudaStream_t st,
                       bool trace) {
     const long long blocks = (rp.G + threads - 1) / threads;
+    if (rp.ws && !trace) {  // warp-specialised: 32 trajectories per 2-warp CTA (ssa_thread_ws.cuh)
+        auto k = ssa_thread_ws_kernel<S, M>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<(unsigned)((rp.G + 31) / 32), 64, smem, st>>>(rp, tt);
+        return cudaGetLastError();
+    }
     if (trace) {
         auto k = ssa_thread_kernel<S, M, true>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

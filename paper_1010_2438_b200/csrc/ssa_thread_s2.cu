@@ -1,6 +1,7 @@
 // ssa_thread_s2.cu -- thread-path instantiations for 2 padded cell(s)
 // (split per cell count so the variants compile in parallel).
 #include "ssa_thread_impl.cuh"
+#include "ssa_thread_ws.cuh"
 
 namespace cwc {
 template cudaError_t launch_s<2>(int, const RunParams &, const ThreadTables &, int, size_t, cudaStream_t, bool);

@@ -1,6 +1,7 @@
 // ssa_thread_s4.cu -- thread-path instantiations for 4 padded cell(s)
 // (split per cell count so the variants compile in parallel).
 #include "ssa_thread_impl.cuh"
+#include "ssa_thread_ws.cuh"
 
 namespace cwc {
 template cudaError_t launch_s<4>(int, const RunParams &, const ThreadTables &, int, size_t, cudaStream_t, bool);

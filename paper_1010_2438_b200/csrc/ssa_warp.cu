@@ -52,13 +52,27 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
     return v;
 }
 
-template <bool TRACE>
-__global__ void __launch_bounds__(128, 6) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
+// Inclusive scan of lanes [0, w) (w a power of two <= 32, warp-uniform);
+// lanes >= w get garbage that callers mask out.
+__device__ __forceinline__ double warp_incl_scan_w(double v, int lane, int w) {
+    for (int d = 1; d < w; d <<= 1) {
+        const double y = __shfl_up_sync(kFull, v, d);
+        if (lane >= d) v = __dadd_rn(y, v);
+    }
+    return v;
+}
+
+// MINB: CTAs per SM the register allocation must allow (8 -> 64 registers,
+// for models whose per-warp shared memory lets 8 CTAs reside; 6 -> 80).
+template <bool TRACE, int MINB>
+__global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
                                                        int per_warp_bytes, int x_bytes) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     const int B = wt.B, Bp = wt.Bp;
+    int scan_w = 1;  // in-chunk scan width: next power of two >= min(B, 32)
+    while (scan_w < B && scan_w < 32) scan_w <<= 1;
     const int O = wt.O;
     const int M = wt.M;
     const long long J = rp.J, J1 = J + 1;
@@ -182,7 +196,7 @@ __global__ void __launch_bounds__(128, 6) ssa_warp_kernel(const RunParams rp, co
             for (int k0 = 0; k0 < B; k0 += 32) {
                 const int k = k0 + lane;
                 const double a = (k < B) ? as[L * Bp + k] : 0.0;
-                const double c = __dadd_rn(carry, warp_incl_scan(a, lane));
+                const double c = __dadd_rn(carry, warp_incl_scan_w(a, lane, scan_w));
                 const unsigned hit = __ballot_sync(kFull, k < B && target < c);
                 const unsigned pos = __ballot_sync(kFull, a > 0.0);
                 if (hit) {
@@ -229,6 +243,7 @@ __global__ void __launch_bounds__(128, 6) ssa_warp_kernel(const RunParams rp, co
             if ((dirty >> lane) & 1u) {
                 const double *ch = as + lane * Bp;
                 double s = ch[0];
+#pragma unroll 4
                 for (int k = 1; k < B; ++k) s = __dadd_rn(s, ch[k]);
                 part = s;
             }
@@ -270,7 +285,9 @@ cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int block
     const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
     const int x_bytes = align16(4ll * (wt.n_cells + 1));
     const int per_warp = (int)warp_smem_per_warp(wt);
-    auto k = (rp.n_trace > 0) ? ssa_warp_kernel<true> : ssa_warp_kernel<false>;
+    const bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
+    auto k = (rp.n_trace > 0) ? (small ? ssa_warp_kernel<true, 8> : ssa_warp_kernel<true, 6>)
+                              : (small ? ssa_warp_kernel<false, 8> : ssa_warp_kernel<false, 6>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);
