@@ -261,6 +261,22 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
                 pack |= (uint64_t)(uint8_t)(int8_t)m->nu_delta[q] << (8 * m->nu_cell[q]);
             tt.nu_pack[k] = pack;
         }
+        // operand deltas (read by the kernel only when M <= 4)
+        for (int k = 0; k < M; ++k) {
+            auto delta_of = [&](int cell) {
+                int dlt = 0;
+                for (int q = m->nu_ptr[k]; q < m->nu_ptr[k + 1]; ++q)
+                    if (m->nu_cell[q] == cell) dlt = m->nu_delta[q];
+                return dlt;
+            };
+            uint64_t op = 0;
+            for (int r2 = 0; r2 < M && r2 < 4; ++r2) {
+                const int ia = tt.ia[r2], ib = tt.ib[r2];
+                op |= (uint64_t)(uint8_t)(int8_t)(ia >= 0 ? delta_of(ia) : 0) << (16 * r2);
+                op |= (uint64_t)(uint8_t)(int8_t)(ib >= 0 ? delta_of(ib) : 0) << (16 * r2 + 8);
+            }
+            tt.op_pack[k] = op;
+        }
         for (int c = 0; c < kThreadMaxCells; ++c) {
             tt.obs_of[c] = c < ncell ? m->obs_of_cell[c] : -1;
             tt.init[c] = c < ncell ? m->init[c] : 0;

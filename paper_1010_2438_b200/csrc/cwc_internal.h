@@ -106,6 +106,10 @@ struct ThreadTables {
     int32_t ia[kThreadMaxReactions], ib[kThreadMaxReactions];
     int32_t sub[kThreadMaxReactions], shr[kThreadMaxReactions];
     uint64_t nu_pack[kThreadMaxReactions];   // int8 delta per cell
+    // M <= 4: int8 delta of every reaction operand (byte 2m: x[ia_m], byte
+    // 2m+1: x[ib_m]; 0 for an absent reactant) -- the kernel then keeps the
+    // operands themselves as state instead of gathering them from x
+    uint64_t op_pack[kThreadMaxReactions];
     int32_t obs_of[kThreadMaxCells];
     int32_t init[kThreadMaxCells];
 };

@@ -53,13 +53,47 @@ __device__ __forceinline__ int pick(const int (&x)[S], int idx) {
     return v;
 }
 
+// Reactant gather x[ia[m]] as bit masks built once per thread (the indices
+// are uniform, but 2*M*S compares do not fit in the predicate registers and
+// would be re-evaluated every firing): xa = oa | OR_s (x[s] & ma[s]), where
+// ma[s] = -1 iff ia == s and oa = 1 for an absent reactant (the constant 1).
+template <int S, int M>
+struct Gather {
+    int ma[M][S], mb[M][S];
+    int oa[M], ob[M];
+    __device__ __forceinline__ explicit Gather(const ThreadTables &tt) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            oa[m] = tt.ia[m] < 0 ? 1 : 0;
+            ob[m] = tt.ib[m] < 0 ? 1 : 0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                ma[m][s] = tt.ia[m] == s ? -1 : 0;
+                mb[m][s] = tt.ib[m] == s ? -1 : 0;
+            }
+        }
+    }
+    __device__ __forceinline__ int a(const int (&x)[S], int m) const {
+        int v = oa[m];
+#pragma unroll
+        for (int s = 0; s < S; ++s) v |= x[s] & ma[m][s];
+        return v;
+    }
+    __device__ __forceinline__ int b(const int (&x)[S], int m) const {
+        int v = ob[m];
+#pragma unroll
+        for (int s = 0; s < S; ++s) v |= x[s] & mb[m][s];
+        return v;
+    }
+};
+
 // cum_m = sum_{i<=m} a_i, left to right (== the oracle's a0 order).
 template <int S, int M>
-__device__ __forceinline__ void cumulative(const ThreadTables &tt, const int (&x)[S], const double (&c)[M],
-                                           double (&cum)[M]) {
+__device__ __forceinline__ void cumulative(const ThreadTables &tt, const Gather<S, M> &gt, const int (&x)[S],
+                                           const double (&c)[M], double (&cum)[M]) {
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-        const double a = __dmul_rn(c[m], combos(pick(x, tt.ia[m]), pick(x, tt.ib[m]), tt.sub[m], tt.shr[m]));
+        const double a = __dmul_rn(c[m], combos(gt.a(x, m), gt.b(x, m), tt.sub[m], tt.shr[m]));
         cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
     }
 }
@@ -92,6 +126,66 @@ __device__ __forceinline__ bool apply_nu(const int (&x)[S], unsigned long long n
     return wrapped;
 }
 
+// One speculative firing of the fast batch: propensities, a0, tau and the
+// selection, update applied at once; returns whether the firing was "plain"
+// (fast division valid -- a0 > 0 and in range --, no sample crossed, no count
+// left int32).  For M <= 4 the reaction operands x[ia_m], x[ib_m] are kept as
+// state and updated through op_pack (one compare chain selects both packed
+// deltas), so the serial chain never gathers from x.
+template <int S, int M>
+struct FastChain {
+    static constexpr bool OPND = (M <= 4);
+    int A[M], Bo[M];
+
+    __device__ __forceinline__ void load(const ThreadTables &tt, const int (&x)[S]) {
+        if constexpr (OPND) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                A[m] = pick(x, tt.ia[m]);
+                Bo[m] = pick(x, tt.ib[m]);
+            }
+        }
+    }
+
+    __device__ __forceinline__ bool step(const ThreadTables &tt, const Gather<S, M> &gt, const double (&c)[M],
+                                         int (&x)[S], double &t, double E, double U, double t_next) {
+        double cum[M];
+        if constexpr (OPND) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const double a = __dmul_rn(c[m], combos(A[m], Bo[m], tt.sub[m], tt.shr[m]));
+                cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
+            }
+        } else {
+            cumulative(tt, gt, x, c, cum);
+        }
+        const double a0 = cum[M - 1];
+        const double tn = __dadd_rn(t, div_fast(E, a0));
+        const double target = __dmul_rn(U, a0);
+        unsigned long long nu = tt.nu_pack[0], op = tt.op_pack[0];
+#pragma unroll
+        for (int m = 0; m + 1 < M; ++m) {
+            const bool past = cum[m] <= target;
+            nu = past ? tt.nu_pack[m + 1] : nu;
+            if constexpr (OPND) op = past ? tt.op_pack[m + 1] : op;
+        }
+        int xn[S];
+        const bool wrapped = apply_nu(x, nu, xn);
+        const bool ok = div_fast_ok(E, a0) && (tn < t_next) && !wrapped;
+#pragma unroll
+        for (int s = 0; s < S; ++s) x[s] = xn[s];
+        t = tn;
+        if constexpr (OPND) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                A[m] += (int)(signed char)(unsigned char)(op >> (16 * m));
+                Bo[m] += (int)(signed char)(unsigned char)(op >> (16 * m + 8));
+            }
+        }
+        return ok;
+    }
+};
+
 template <int S>
 __device__ __forceinline__ void record_sample(const RunParams &rp, const ThreadTables &tt, const StatAcc &acc,
                                               const int (&x)[S], long long cell_base, long long g, long long j) {
@@ -111,7 +205,7 @@ struct ThreadBatch {
 };
 
 template <int S, int M, bool TRACE>
-__global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
     constexpr int B = ThreadBatch<M>::B;
     extern __shared__ __align__(16) unsigned char smem[];
     const long long T = blockDim.x;
@@ -164,6 +258,9 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
         double c[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
+        const Gather<S, M> gt(tt);
+        FastChain<S, M> fc;
+        fc.load(tt, x);
 
         double t = 0.0, t_next = 0.0;  // t_next = j * dt: sample 0 is crossed by the first firing
         long long j = 0, firings = 0;
@@ -195,22 +292,10 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
-                double cum[M];
-                cumulative(tt, x, c, cum);
-                const double a0 = cum[M - 1];
-                const double tn = __dadd_rn(t, div_fast(Eb[k], a0));
-                int mu;
-                const unsigned long long nu = select_nu<M, false>(tt, cum, __dmul_rn(Ub[k], a0), mu);
-                int xn[S];
-                const bool wrapped = apply_nu(x, nu, xn);
-                // plain: fast division valid (a0 > 0 and in range), no sample
-                // crossed, no count left int32.  TRACE builds take every firing
-                // through the exact path below (it writes the trace).
-                const bool ok = !TRACE && div_fast_ok(Eb[k], a0) && (tn < t_next) && !wrapped;
+                // TRACE builds take every firing through the exact path below
+                // (it writes the trace)
+                const bool ok = fc.step(tt, gt, c, x, t, Eb[k], Ub[k], t_next) && !TRACE;
                 bad |= ok ? 0u : (1u << k);
-#pragma unroll
-                for (int s = 0; s < S; ++s) x[s] = xn[s];
-                t = tn;
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
@@ -237,7 +322,7 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
                 }
                 if (live && bad != 0u) {
                     double cum[M];
-                    cumulative(tt, x, c, cum);
+                    cumulative(tt, gt, x, c, cum);
                     const double a0 = cum[M - 1];
                     if (a0 == 0.0) {  // stall: no draw is consumed
                         for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
@@ -298,6 +383,7 @@ __global__ void __launch_bounds__(256) ssa_thread_kernel(const RunParams rp, con
                         }
                     }
                 }
+                if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
             }
 #pragma unroll
             for (int i = 0; i < B; ++i) {

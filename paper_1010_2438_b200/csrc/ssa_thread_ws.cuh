@@ -16,9 +16,10 @@
 //
 // The two warps of a CTA sit on different SM sub-partitions, so the chain
 // and the RNG issue in parallel.  Hand-off per trajectory: the producer
-// writes slots, fences, then publishes prod[lane]; the consumer reads
-// prod[lane], fences, reads slots, and publishes cons[lane] (the producer
-// refills a slot only after the consumer has released it).  done[lane] ends
+// writes slots, then publishes prod[lane] with a release store; the consumer
+// reads prod[lane] with an acquire load, reads the slots, and publishes
+// cons[lane] with a release store (the producer acquires it before refilling
+// a slot).  done[lane] ends
 // the producer's work for that trajectory.  Both warps belong to one CTA, so
 // both are resident and each always makes progress once the other has.
 #pragma once
@@ -27,11 +28,19 @@
 namespace cwc {
 
 
-__device__ __forceinline__ unsigned ld_vol(const unsigned *p) { return *(const volatile unsigned *)p; }
-__device__ __forceinline__ void st_vol(unsigned *p, unsigned v) { *(volatile unsigned *)p = v; }
+// CTA-scope acquire / release on the hand-off counters (lighter than a full
+// sequentially-consistent fence: they order only what the protocol needs)
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
+    asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int S, int M>
-__global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
     constexpr int B = ThreadBatch<M>::B;
     constexpr int K = kWsRing;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -75,9 +84,9 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
         // ---------------- producer ----------------
         unsigned long long p = 0;  // draws produced (prod/cons hold its low 32 bits; differences wrap)
         for (;;) {
-            const bool act = ld_vol(done + lane) == 0u;
+            const bool act = ld_acquire(done + lane) == 0u;
             if (!__any_sync(0xffffffffu, act)) break;
-            const unsigned c = ld_vol(cons + lane);
+            const unsigned c = ld_acquire(cons + lane);
             const bool room = act && ((unsigned)p + 4u - c <= (unsigned)K);
             if (__any_sync(0xffffffffu, room)) {
                 DrawPipe<4> pipe;
@@ -92,9 +101,8 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
                         ringE[slot * 32 + lane] = E4[i];
                         ringU[slot * 32 + lane] = U4[i];
                     }
-                    __threadfence_block();
                     p += 4;
-                    st_vol(prod + lane, (unsigned)p);
+                    st_release(prod + lane, (unsigned)p);
                 }
             } else {
                 __nanosleep(100);
@@ -111,6 +119,9 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
         double c[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
+        const Gather<S, M> gt(tt);
+        FastChain<S, M> fc;
+        fc.load(tt, x);
 
         double t = 0.0, t_next = 0.0;
         long long j = 0, firings = 0;
@@ -120,11 +131,10 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
         while (__any_sync(0xffffffffu, live)) {
             // draws n .. n+B-1 of every live lane must be published
             for (;;) {
-                const bool short_ = live && ((int)(ld_vol(prod + lane) - (unsigned)(n + B)) < 0);
+                const bool short_ = live && ((int)(ld_acquire(prod + lane) - (unsigned)(n + B)) < 0);
                 if (!__any_sync(0xffffffffu, short_)) break;
                 __nanosleep(20);
             }
-            __threadfence_block();
             double Eb[B], Ub[B];
 #pragma unroll
             for (int k = 0; k < B; ++k) {
@@ -142,19 +152,8 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
-                double cum[M];
-                cumulative(tt, x, c, cum);
-                const double a0 = cum[M - 1];
-                const double tn = __dadd_rn(t, div_fast(Eb[k], a0));
-                int mu;
-                const unsigned long long nu = select_nu<M, false>(tt, cum, __dmul_rn(Ub[k], a0), mu);
-                int xn[S];
-                const bool wrapped = apply_nu(x, nu, xn);
-                const bool ok = div_fast_ok(Eb[k], a0) && (tn < t_next) && !wrapped;
+                const bool ok = fc.step(tt, gt, c, x, t, Eb[k], Ub[k], t_next);
                 bad |= ok ? 0u : (1u << k);
-#pragma unroll
-                for (int s = 0; s < S; ++s) x[s] = xn[s];
-                t = tn;
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;
@@ -180,7 +179,7 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
                 }
                 if (live && bad != 0u) {
                     double cum[M];
-                    cumulative(tt, x, c, cum);
+                    cumulative(tt, gt, x, c, cum);
                     const double a0 = cum[M - 1];
                     if (a0 == 0.0) {  // stall
                         for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
@@ -215,11 +214,11 @@ __global__ void __launch_bounds__(64) ssa_thread_ws_kernel(const RunParams rp, c
                         }
                     }
                 }
+                if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
             }
-            // release consumed slots (reads above happen before the store)
-            __threadfence_block();
-            st_vol(cons + lane, (unsigned)n);
-            if (in_range && !live) st_vol(done + lane, 1u);
+            // release consumed slots (the slot reads above are ordered before it)
+            st_release(cons + lane, (unsigned)n);
+            if (in_range && !live) st_release(done + lane, 1u);
             asm volatile("bar.warp.sync -1;" ::: "memory");
         }
         if (in_range) {
