@@ -344,7 +344,7 @@ struct Plan {
     int64_t traj_per_part = 0;
     size_t smem_bytes = 0;
     // workspace layout
-    size_t off_rates = 0, off_parts = 0, off_trace = 0, off_counter = 0, off_stats = 0, total = 0;
+    size_t off_rates = 0, off_parts = 0, off_trace = 0, off_counter = 0, off_order = 0, off_stats = 0, total = 0;
 };
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -409,10 +409,11 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // refills SMs as warps finish; the thread path is latency-bound, so
         // nothing is gained from larger CTAs
         int T = bt ? bt : 32;
-        // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories)
-        // when the consumer warps alone leave sub-partitions idle
+        // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories;
+        // ssa_thread_ws.cuh); the single-warp kernel serves traced runs and
+        // explicit block sizes
         const bool tracing = opts && opts->n_trace > 0;
-        bool ws = !tracing && !bt && (pl.G + 31) / 32 <= 4ll * nsm;
+        bool ws = !tracing && !bt;
         if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
         if (ws) T = 32;
         pl.ws = ws ? 1 : 0;
@@ -511,6 +512,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     off = align256(off + sizeof(int64_t) * (size_t)std::max(opts ? opts->n_trace : 0, 1));
     pl.off_counter = off;
     off = align256(off + 16);
+    pl.off_order = off;
+    if (pl.path == CWC_PATH_THREAD && pl.P > 1) off = align256(off + sizeof(int32_t) * (size_t)pl.blocks);
     pl.off_stats = off;
     if (host_stats) off = align256(off + (size_t)32 * std::max<int64_t>(pl.n_stat_cells, 1));
     pl.total = off;
@@ -593,6 +596,40 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     if (!pl.stats_smem) {
         e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: zero partials");
+    }
+    if (pl.path == CWC_PATH_THREAD && pl.P > 1) {
+        // Parameter sweeps: trajectory lengths differ by point (C3: 17x), and
+        // CTAs start in blockIdx order as the SMs free up.  Dispatch the
+        // groups longest-expected-first (LPT), estimating a group's work by
+        // the total propensity a0(x0) of its trajectories' points (firings per
+        // unit time at t = 0).  Trajectory ids -- hence the RNG streams and
+        // every result -- are unchanged; only the start order moves.
+        std::vector<double> a0p(pl.P, 0.0);
+        for (int p = 0; p < pl.P; ++p) {
+            double a0 = 0.0;
+            for (int k = 0; k < M; ++k) {
+                const ReactionDesc &r = m->rx[k];
+                const double xa = r.ia < m->n_cells ? (double)m->init[r.ia] : 1.0;
+                const double xb = r.ib < m->n_cells ? (double)m->init[r.ib] - (r.kind & 1) : 1.0;
+                a0 += rates[(size_t)p * M + k] * xa * xb / ((r.kind >> 1) ? 2.0 : 1.0);
+            }
+            a0p[p] = a0;
+        }
+        const int T = pl.ws ? 32 : pl.threads;
+        std::vector<std::pair<double, int32_t>> w8(pl.blocks);
+        for (int b = 0; b < pl.blocks; ++b) {
+            double s = 0.0;
+            const int64_t ge = std::min<int64_t>((int64_t)(b + 1) * T, pl.G);
+            for (int64_t gg = (int64_t)b * T; gg < ge; ++gg) s += a0p[gg / pl.R];
+            w8[b] = {-s, b};
+        }
+        std::stable_sort(w8.begin(), w8.end());
+        // pageable source: cudaMemcpyAsync has copied it when it returns
+        std::vector<int32_t> order_host(pl.blocks);
+        for (int b = 0; b < pl.blocks; ++b) order_host[b] = w8[b].second;
+        e = cudaMemcpyAsync(w + pl.off_order, order_host.data(), sizeof(int32_t) * pl.blocks, cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: dispatch order upload");
+        rp.cta_order = (const int32_t *)(w + pl.off_order);
     }
     e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: counter");

@@ -149,6 +149,15 @@ struct FastChain {
 
     __device__ __forceinline__ bool step(const ThreadTables &tt, const Gather<S, M> &gt, const double (&c)[M],
                                          int (&x)[S], double &t, double E, double U, double t_next) {
+        bool cross1;
+        return step2(tt, gt, c, x, t, E, U, t_next, t_next, cross1);
+    }
+
+    // As step(); additionally cross1 = the firing crossed exactly one sample
+    // time (t_next <= t + tau < t_next2) and is otherwise plain.
+    __device__ __forceinline__ bool step2(const ThreadTables &tt, const Gather<S, M> &gt, const double (&c)[M],
+                                          int (&x)[S], double &t, double E, double U, double t_next, double t_next2,
+                                          bool &cross1) {
         double cum[M];
         if constexpr (OPND) {
 #pragma unroll
@@ -171,7 +180,9 @@ struct FastChain {
         }
         int xn[S];
         const bool wrapped = apply_nu(x, nu, xn);
-        const bool ok = div_fast_ok(E, a0) && (tn < t_next) && !wrapped;
+        const bool valid = div_fast_ok(E, a0) && !wrapped;
+        const bool ok = valid && (tn < t_next);
+        cross1 = valid && !(tn < t_next) && (tn < t_next2);
 #pragma unroll
         for (int s = 0; s < S; ++s) x[s] = xn[s];
         t = tn;
@@ -209,7 +220,9 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
     constexpr int B = ThreadBatch<M>::B;
     extern __shared__ __align__(16) unsigned char smem[];
     const long long T = blockDim.x;
-    const long long g0 = (long long)blockIdx.x * T;
+    // dispatch order: CTA slot blockIdx.x runs trajectory group cta (RunParams.cta_order)
+    const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
+    const long long g0 = cta * T;
     const long long g = g0 + threadIdx.x;
     const int O = tt.O;
     const long long J = rp.J;
@@ -225,7 +238,7 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
         p_base = g0 / rp.R;
         __syncthreads();
     } else {
-        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
+        acc = stat_view((unsigned char *)rp.parts + (cta % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
                         rp.cells_per_part, rp.st);
     }
 
@@ -406,7 +419,7 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
     if (rp.stats_smem) {  // coalesced, vectorised flush of the block's partial moments
         __syncthreads();
         const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
-        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.st, rp.cells_per_part));
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + cta * stat_bytes(rp.st, rp.cells_per_part));
         const uint4 *src = (const uint4 *)smem;
         for (long long i = threadIdx.x; i < n16; i += T) dst[i] = src[i];
     }

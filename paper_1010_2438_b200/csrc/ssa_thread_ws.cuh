@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const long long g0 = (long long)blockIdx.x * 32;
+    // dispatch order: CTA slot blockIdx.x runs trajectory group cta (RunParams.cta_order)
+    const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
+    const long long g0 = cta * 32;
     const long long g = g0 + lane;
     const int O = tt.O;
     const long long J = rp.J;
@@ -58,6 +60,8 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
     unsigned *prod = (unsigned *)(ringU + K * 32);     // [32] draws published
     unsigned *cons = prod + 32;                        // [32] draws released
     unsigned *done = cons + 32;                        // [32] trajectory finished
+    long long *st_cell = (long long *)(done + 32);     // [kWsStage] first cell of a staged record
+    long long *st_v = st_cell + kWsStage;              // [kWsStage][kThreadMaxObs] its observables
 
     StatAcc acc;
     long long p_base = 0;
@@ -67,7 +71,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
         for (long long i = threadIdx.x; i < stats_bytes / 16; i += 64) z[i] = make_uint4(0, 0, 0, 0);
         p_base = g0 / rp.R;
     } else {
-        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
+        acc = stat_view((unsigned char *)rp.parts + (cta % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
                         rp.cells_per_part, rp.st);
     }
     const bool in_range = g < rp.G;
@@ -123,7 +127,8 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
         FastChain<S, M> fc;
         fc.load(tt, x);
 
-        double t = 0.0, t_next = 0.0;
+        int stage_n = 0;  // staged records (warp-uniform)
+        double t = 0.0, t_next = 0.0, t_next2 = rp.dt;  // t_next = j*dt, t_next2 = (j+1)*dt
         long long j = 0, firings = 0;
         unsigned long long n = 0;
         int status = 0;
@@ -143,23 +148,74 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
                 Ub[k] = ringU[slot * 32 + lane];
             }
 
-            // ---- fast batch (speculative, as ssa_thread_kernel) ----
+            // ---- fast batch (speculative, as ssa_thread_kernel); one firing
+            // per batch may also cross a single sample time that is not the
+            // last: it commits, and its record (pre-event state xrec, sample
+            // jrec) is written after the batch ----
             int xsnap[B][S];
             double tsnap[B];
             unsigned bad = 0;
+            bool rec = false;
+            int krec = B;
+            long long jrec = 0;
+            int xrec[S];
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
-                const bool ok = fc.step(tt, gt, c, x, t, Eb[k], Ub[k], t_next);
-                bad |= ok ? 0u : (1u << k);
+                bool cross1;
+                const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
+                const bool take = cross1 && !rec && (j < J);
+                if (take) {
+                    rec = true;
+                    krec = k;
+                    jrec = j;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) xrec[s] = xsnap[k][s];
+                    j += 1;
+                    t_next = t_next2;
+                    t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+                }
+                bad |= (plain || take) ? 0u : (1u << k);
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;
+            if (rec && krec >= used) {  // the crossing firing was rolled back
+                rec = false;
+                j = jrec;
+                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+            }
             if (live) {
                 n += (unsigned long long)used;
                 firings += used;
+            }
+            // Sample records of the batch are staged in shared memory and
+            // written 32 at a time, one per lane: the fire-and-forget limb
+            // atomics of a record then run with the whole warp active instead
+            // of one lane at a time.
+            const unsigned rmask = __ballot_sync(0xffffffffu, rec);
+            if (rmask) {
+                if (rec) {
+                    const int slot = stage_n + __popc(rmask & ((1u << lane) - 1u));
+                    st_cell[slot] = cell_base + jrec * O;
+                    for (int o = 0; o < O; ++o) {
+                        long long v = 0;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)xrec[s] : 0ll;
+                        st_v[slot * kThreadMaxObs + o] = v;
+                        if (rp.out_traj) rp.out_traj[(g * J1 + jrec) * O + o] = v;
+                    }
+                }
+                stage_n += __popc(rmask);
+                if (stage_n >= 32) {
+                    __syncwarp();
+                    const int e = stage_n - 32 + lane;
+                    for (int o = 0; o < O; ++o) stat_record(acc, st_cell[e] + o, st_v[e * kThreadMaxObs + o]);
+                    stage_n -= 32;
+                    __syncwarp();
+                }
             }
 
             // ---- rare: roll back, one exact iteration ----
@@ -197,6 +253,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
                             live = false;
                         } else {
                             t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                            t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
                             int mu;
                             const unsigned long long nu = select_nu<M, false>(tt, cum, __dmul_rn(u2, a0), mu);
                             int xn[S];
@@ -221,6 +278,9 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
             if (in_range && !live) st_release(done + lane, 1u);
             asm volatile("bar.warp.sync -1;" ::: "memory");
         }
+        __syncwarp();
+        if (lane < stage_n)  // drain the staged records
+            for (int o = 0; o < O; ++o) stat_record(acc, st_cell[lane] + o, st_v[lane * kThreadMaxObs + o]);
         if (in_range) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
@@ -230,7 +290,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
     if (rp.stats_smem) {
         __syncthreads();
         const long long n16 = stats_bytes / 16;
-        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stats_bytes);
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + cta * stats_bytes);
         const uint4 *src = (const uint4 *)smem;
         for (long long i = threadIdx.x; i < n16; i += 64) dst[i] = src[i];
     }
