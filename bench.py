@@ -113,7 +113,7 @@ def _peaks():
         return {}
 
 
-def _ncu_traffic(config, kernel_prefix):
+def _ncu_traffic(config, kernel_prefix):  # kernel_prefix: substring of the ncu kernel name
     """DRAM bytes per launch of the SSA kernel from the committed ncu capture of
     this config's bench launch (profiles/ncu_bench.json, written by
     tools/ncu_summary.py from an `ncu --set full` run of tools/run_case.py at
@@ -121,7 +121,7 @@ def _ncu_traffic(config, kernel_prefix):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_bench.json")) as f:
             d = json.load(f).get(config)
-        if d and str(d.get("kernel", "")).startswith(kernel_prefix):
+        if d and kernel_prefix in str(d.get("kernel", "")):
             return float(d["dram_bytes"])
     except Exception:
         pass
@@ -317,8 +317,7 @@ def run_ours(args):
     achieved = ops * fired / (k_ms / 1e3)
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
                 "frac": achieved / peak_ops,
-                "traffic": _ncu_traffic(args.config, "void cwc::ssa_thread_kernel" if path == "thread"
-                                        else "void cwc::ssa_warp_kernel"),
+                "traffic": _ncu_traffic(args.config, "ssa_thread" if path == "thread" else "ssa_warp_kernel"),
                 "ops_per_firing": ops, "kernel": "ssa_%s_kernel" % path, "kernel_ms": k_ms,
                 "peak_source": "issue peak = %d SMs x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
                 % (props.multi_processor_count, f_max / 1e6)}

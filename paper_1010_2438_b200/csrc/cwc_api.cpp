@@ -382,7 +382,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         pl.P = sweep->n_points;
     }
     pl.R = n_replicas;
-    if ((double)pl.P * (double)n_replicas > 9e18 / 2) return fail(CWC_ERR_INVALID, "too many trajectories");
+    if ((double)pl.P * (double)n_replicas >= 4294967296.0)  // statistics words take < 2^32 adds
+        return fail(CWC_ERR_INVALID, "too many trajectories in one call (shard the run: replica_offset)");
     pl.G = (int64_t)pl.P * n_replicas;
     const int64_t J1 = (int64_t)pl.J + 1;
     const int O = m->n_obs;
@@ -448,9 +449,9 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             pl.stats_smem = 0;
             pl.st = lay_g;
             pl.cells_per_part = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
-            const int64_t budget = (int64_t)256 << 20;
-            int64_t np = (pl.R <= 64) ? 1 : std::min<int64_t>(blocks, std::max<int64_t>(1, budget / stat_bytes(pl.st, pl.cells_per_part)));
-            pl.n_parts = (int)np;
+            // one global part: its 64-bit words take 2^32 adds of 32-bit limbs
+            // (G < 2^32), and crossings are far too rare to contend in L2
+            pl.n_parts = 1;
             pl.traj_per_part = 0;
             pl.smem_bytes = extra;
         }
@@ -497,8 +498,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         if (use_smem) {
             pl.n_parts = pl.blocks;
         } else {
-            const int64_t budget = (int64_t)512 << 20;
-            pl.n_parts = (int)std::min<int64_t>(pl.blocks, std::max<int64_t>(1, budget / stat_bytes(pl.st, cells)));
+            pl.n_parts = 1;  // one global part (see the thread path)
         }
     }
 

@@ -28,6 +28,8 @@
 //   (precomputed slots) and only their owner lanes re-sum their chunks.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "cwc_internal.h"
 #include "device_common.cuh"
 
@@ -53,18 +55,38 @@ __device__ __forceinline__ double warp_incl_scan(double v, int lane) {
 }
 
 // Inclusive scan of lanes [0, w) (w a power of two <= 32, warp-uniform);
-// lanes >= w get garbage that callers mask out.
+// lanes >= w get garbage that callers mask out.  Unrolled; the steps at or
+// beyond w are skipped by a warp-uniform test.
 __device__ __forceinline__ double warp_incl_scan_w(double v, int lane, int w) {
-    for (int d = 1; d < w; d <<= 1) {
-        const double y = __shfl_up_sync(kFull, v, d);
-        if (lane >= d) v = __dadd_rn(y, v);
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        if (d < w) {
+            const double y = __shfl_up_sync(kFull, v, d);
+            if (lane >= d) v = __dadd_rn(y, v);
+        }
     }
     return v;
 }
 
+// Left-to-right sum of a chunk of B entries; BMAX > 0: compile-time bound
+// (B <= BMAX), fully unrolled.
+template <int BMAX>
+__device__ __forceinline__ double chunk_sum(const double *ch, int B) {
+    double s = ch[0];
+    if constexpr (BMAX > 0) {
+#pragma unroll
+        for (int k = 1; k < BMAX; ++k)
+            if (k < B) s = __dadd_rn(s, ch[k]);
+    } else {
+#pragma unroll 4
+        for (int k = 1; k < B; ++k) s = __dadd_rn(s, ch[k]);
+    }
+    return s;
+}
+
 // MINB: CTAs per SM the register allocation must allow (8 -> 64 registers,
 // for models whose per-warp shared memory lets 8 CTAs reside; 6 -> 80).
-template <bool TRACE, int MINB>
+template <bool TRACE, int MINB, int BMAX>
 __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
                                                        int per_warp_bytes, int x_bytes) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -240,13 +262,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             }
             dirty = __reduce_or_sync(kFull, dirty);
             __syncwarp();
-            if ((dirty >> lane) & 1u) {
-                const double *ch = as + lane * Bp;
-                double s = ch[0];
-#pragma unroll 4
-                for (int k = 1; k < B; ++k) s = __dadd_rn(s, ch[k]);
-                part = s;
-            }
+            if ((dirty >> lane) & 1u) part = chunk_sum<BMAX>(as + lane * Bp, B);
             incl = warp_incl_scan(part, lane);
             a0 = shfl_d(incl, 31);
             excl = __shfl_up_sync(kFull, incl, 1);
@@ -286,8 +302,13 @@ cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int block
     const int x_bytes = align16(4ll * (wt.n_cells + 1));
     const int per_warp = (int)warp_smem_per_warp(wt);
     const bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
-    auto k = (rp.n_trace > 0) ? (small ? ssa_warp_kernel<true, 8> : ssa_warp_kernel<true, 6>)
-                              : (small ? ssa_warp_kernel<false, 8> : ssa_warp_kernel<false, 6>);
+    auto pick = [&](auto tr) {
+        constexpr bool T = decltype(tr)::value;
+        if (wt.B <= 8) return small ? ssa_warp_kernel<T, 8, 8> : ssa_warp_kernel<T, 6, 8>;
+        if (wt.B <= 16) return small ? ssa_warp_kernel<T, 8, 16> : ssa_warp_kernel<T, 6, 16>;
+        return small ? ssa_warp_kernel<T, 8, 0> : ssa_warp_kernel<T, 6, 0>;
+    };
+    auto k = (rp.n_trace > 0) ? pick(std::true_type{}) : pick(std::false_type{});
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);
