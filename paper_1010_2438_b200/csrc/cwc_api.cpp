@@ -344,7 +344,8 @@ struct Plan {
     int64_t traj_per_part = 0;
     size_t smem_bytes = 0;
     // workspace layout
-    size_t off_rates = 0, off_parts = 0, off_trace = 0, off_counter = 0, off_order = 0, off_stats = 0, total = 0;
+    size_t off_rates = 0, off_parts = 0, off_trace = 0, off_counter = 0, off_order = 0, off_smctr = 0, off_stats = 0,
+           total = 0;
 };
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -416,7 +417,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const bool tracing = opts && opts->n_trace > 0;
         bool ws = !tracing && !bt;
         if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
-        if (ws) T = 32;
+        if (ws) T = 32 * kWsGroups;
         pl.ws = ws ? 1 : 0;
         pl.threads = T;
         const int64_t blocks = (pl.G + T - 1) / T;
@@ -514,6 +515,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     off = align256(off + 16);
     pl.off_order = off;
     if (pl.path == CWC_PATH_THREAD && pl.P > 1) off = align256(off + sizeof(int32_t) * (size_t)pl.blocks);
+    pl.off_smctr = off;
+    if (pl.ws) off = align256(off + sizeof(unsigned) * 1024);
     pl.off_stats = off;
     if (host_stats) off = align256(off + (size_t)32 * std::max<int64_t>(pl.n_stat_cells, 1));
     pl.total = off;
@@ -569,6 +572,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.n_parts = pl.n_parts;
     rp.traj_per_part = pl.traj_per_part;
     rp.next_traj = (unsigned long long *)(w + pl.off_counter);
+    if (const char *e = env("CWC_PROF_PTR")) rp.prof = (unsigned long long *)std::strtoull(e, nullptr, 0);  // debug hook
     if (opts) {
         if (opts->replicas_total != 0) {
             if (opts->replica_offset < 0 || opts->replicas_total < opts->replica_offset + n_replicas)
@@ -615,7 +619,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
             }
             a0p[p] = a0;
         }
-        const int T = pl.ws ? 32 : pl.threads;
+        const int T = pl.ws ? 32 * kWsGroups : pl.threads;
         std::vector<std::pair<double, int32_t>> w8(pl.blocks);
         for (int b = 0; b < pl.blocks; ++b) {
             double s = 0.0;
@@ -630,6 +634,15 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         e = cudaMemcpyAsync(w + pl.off_order, order_host.data(), sizeof(int32_t) * pl.blocks, cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: dispatch order upload");
         rp.cta_order = (const int32_t *)(w + pl.off_order);
+    }
+    // Alternating consumer/producer placement per SM (CWC_WS_MIX=1) was
+    // measured slower on C2: a producer's fp64-heavy log stream on the same
+    // sub-partition delays the consumer's fp64 chain more than a second
+    // consumer does.  Kept as an experiment switch.
+    if (pl.ws && env("CWC_WS_MIX") && std::atoi(env("CWC_WS_MIX")) != 0) {
+        e = cudaMemsetAsync(w + pl.off_smctr, 0, sizeof(unsigned) * 1024, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: SM counters");
+        rp.sm_ctr = (unsigned *)(w + pl.off_smctr);
     }
     e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: counter");

@@ -46,9 +46,13 @@ __host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, lo
 // warp-specialised thread path (ssa_thread_ws.cuh): draws in flight per
 // trajectory and the ring + hand-off counters' shared-memory bytes per CTA
 constexpr int kWsRing = 32;
-constexpr int kWsStage = 64;  // staged sample records of the consumer warp
-constexpr size_t kWsRingBytes = (size_t)2 * kWsRing * 32 * sizeof(double) + 3 * 32 * sizeof(unsigned) +
-                                (size_t)kWsStage * (1 + kThreadMaxObs) * sizeof(long long);
+constexpr int kWsProducers = 1;  // producer warps per group (2 measured slower on C2)
+constexpr int kWsGroups = 1;     // 32-trajectory groups (consumer + producer warp pairs) per CTA
+constexpr int kWsStage = 64;     // staged sample records of a consumer warp
+constexpr size_t kWsGroupBytes = (size_t)2 * kWsRing * 32 * sizeof(double) +
+                                 (size_t)(kWsProducers + 2) * 32 * sizeof(unsigned) +
+                                 (size_t)kWsStage * (1 + kThreadMaxObs) * sizeof(long long);
+constexpr size_t kWsRingBytes = kWsGroups * ((kWsGroupBytes + 15) & ~(size_t)15);  // per CTA
 constexpr long long kSmemPartMaxTraj = 1ll << 16;  // trajectories per shared-memory part (16-bit limbs)
 __host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }
 // Layout for observables of at most vbits bits (v < 2^vbits, v^2 < 2^(2 vbits)).
@@ -86,6 +90,7 @@ struct RunParams {
     int32_t stats_smem;     // 1: block accumulators in shared memory, flushed to parts[blockIdx]
     int32_t ws;             // thread path: warp-specialised producer/consumer kernel (ssa_thread_ws.cuh)
     const int32_t *cta_order;  // thread path: CTA slot -> trajectory group (NULL = identity)
+    unsigned *sm_ctr;          // warp-specialised kernel: per-SM CTA arrival counters (zeroed per call)
     int32_t part_stride_blocks;  // GLOBAL mode: block b accumulates into part (b % n_parts)
     int32_t n_parts;
     int64_t traj_per_part;  // static mapping: part b covers g in [b*T, (b+1)*T); 0 = all points
@@ -101,6 +106,8 @@ struct RunParams {
     int64_t *trace_len;
     // warp path dynamic scheduling
     unsigned long long *next_traj;
+    // debug: consumer cycle accounting of the warp-specialised kernel (NULL = off)
+    unsigned long long *prof;
 };
 
 // Thread path tables (kernel parameter, constant bank).

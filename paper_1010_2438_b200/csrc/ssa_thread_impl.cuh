@@ -136,6 +136,15 @@ template <int S, int M>
 struct FastChain {
     static constexpr bool OPND = (M <= 4);
     int A[M], Bo[M];
+    // k_m * 2^-shr_m (exact scaling): then a_m = k_m' * RN(x_a (x_b - sub)),
+    // which equals k_m * RN(x_a (x_b - sub) / 2^shr) bit for bit (halving
+    // commutes with rounding), with no 64-bit shift in the chain
+    double ch[M];
+
+    __device__ __forceinline__ void rates(const ThreadTables &tt, const double (&c)[M]) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) ch[m] = tt.shr[m] ? __dmul_rn(c[m], 0.5) : c[m];
+    }
 
     __device__ __forceinline__ void load(const ThreadTables &tt, const int (&x)[S]) {
         if constexpr (OPND) {
@@ -162,7 +171,7 @@ struct FastChain {
         if constexpr (OPND) {
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const double a = __dmul_rn(c[m], combos(A[m], Bo[m], tt.sub[m], tt.shr[m]));
+                const double a = __dmul_rn(ch[m], __ll2double_rn((long long)A[m] * (long long)(Bo[m] - tt.sub[m])));
                 cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
             }
         } else {
@@ -273,6 +282,7 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
         const Gather<S, M> gt(tt);
         FastChain<S, M> fc;
+        fc.rates(tt, c);
         fc.load(tt, x);
 
         double t = 0.0, t_next = 0.0;  // t_next = j * dt: sample 0 is crossed by the first firing
@@ -436,7 +446,7 @@ cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, 
         auto k = ssa_thread_ws_kernel<S, M>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k<<<(unsigned)((rp.G + 31) / 32), 64, smem, st>>>(rp, tt);
+        k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 64 * kWsGroups, smem, st>>>(rp, tt);
         return cudaGetLastError();
     }
     if (trace) {

@@ -28,37 +28,69 @@
 namespace cwc {
 
 
-// CTA-scope acquire / release on the hand-off counters (lighter than a full
-// sequentially-consistent fence: they order only what the protocol needs)
+// Hand-off counters live in shared memory; accesses use the shared state
+// space (LDS/STS, not generic loads).  prod: release store by the producer
+// (its ring writes are ordered before it), acquire load by the consumer.
+// cons/done: plain (relaxed) stores by the consumer -- the ring loads they
+// release have already returned their values (the consumer used them), so no
+// later producer store can affect them; a release here would be a MEMBAR
+// that waits for the consumer's in-flight statistics atomics in L2.
+__device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
-    asm volatile("ld.acquire.cta.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release(unsigned *p, unsigned v) {
-    asm volatile("st.release.cta.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned *p, unsigned v) {
+    asm volatile("st.relaxed.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
 
 template <int S, int M>
-__global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(64 * kWsGroups, 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+    // consumer batch B; one producer warp per group computes rounds of PW
+    // draws (round r = draws [r PW, r PW + PW) of each of its trajectories)
     constexpr int B = ThreadBatch<M>::B;
+    constexpr int PW = 4;
+    constexpr int NP = kWsProducers;
     constexpr int K = kWsRing;
+    constexpr int GPC = kWsGroups;  // 32-trajectory groups per CTA
+    static_assert(K >= B + NP * PW && (K & (K - 1)) == 0 && B <= PW, "ring too small");
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    // dispatch order: CTA slot blockIdx.x runs trajectory group cta (RunParams.cta_order)
+
+    // Roles.  Warp w serves group w / 2, consumer first ([C0 P0 C1 P1 ..]
+    // alternating C/P per pair).  With RunParams.sm_ctr (experiment switch)
+    // the order flips by the parity of the CTA's arrival on its SM, putting a
+    // consumer and a producer on each sub-partition; measured slower on C2
+    // (the producer's fp64 log stream delays the consumer's fp64 chain).
+    __shared__ unsigned pattern;
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pattern = rp.sm_ctr ? (atomicAdd(rp.sm_ctr + (smid & 1023u), 1u) & 1u) : 0u;
+    }
+    __syncthreads();
+    const int grp = warp >> 1;
+    const bool consumer = (((unsigned)(warp & 1) ^ (unsigned)grp) & 1u) == pattern;
+
+    // dispatch order: CTA slot blockIdx.x runs trajectory block cta (RunParams.cta_order)
     const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
-    const long long g0 = cta * 32;
-    const long long g = g0 + lane;
+    const long long g0 = cta * (32 * GPC);
+    const long long g = g0 + grp * 32 + lane;
     const int O = tt.O;
     const long long J = rp.J;
     const long long J1 = J + 1;
 
     const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
-    double *ringE = (double *)(smem + stats_bytes);    // [K][32]
+    unsigned char *gbase = smem + stats_bytes + (long long)grp * (kWsRingBytes / GPC);
+    double *ringE = (double *)gbase;                   // [K][32]
     double *ringU = ringE + K * 32;                    // [K][32]
-    unsigned *prod = (unsigned *)(ringU + K * 32);     // [32] draws published
-    unsigned *cons = prod + 32;                        // [32] draws released
+    unsigned *prod = (unsigned *)(ringU + K * 32);     // [NP][32] rounds published per producer
+    unsigned *cons = prod + NP * 32;                   // [32] draws released
     unsigned *done = cons + 32;                        // [32] trajectory finished
     long long *st_cell = (long long *)(done + 32);     // [kWsStage] first cell of a staged record
     long long *st_v = st_cell + kWsStage;              // [kWsStage][kThreadMaxObs] its observables
@@ -68,7 +100,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
     if (rp.stats_smem) {
         acc = stat_view(smem, rp.cells_per_part, rp.st);
         uint4 *z = (uint4 *)smem;
-        for (long long i = threadIdx.x; i < stats_bytes / 16; i += 64) z[i] = make_uint4(0, 0, 0, 0);
+        for (long long i = threadIdx.x; i < stats_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
         p_base = g0 / rp.R;
     } else {
         acc = stat_view((unsigned char *)rp.parts + (cta % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
@@ -77,36 +109,39 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
     const bool in_range = g < rp.G;
     const long long gc = in_range ? g : rp.G - 1;
     const uint64_t gk = (uint64_t)global_traj(gc, rp.R, rp.R_total, rp.r_off);  // RNG stream id
-    if (warp == 0) {
-        prod[lane] = 0;
+    if (consumer) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) prod[q * 32 + lane] = 0;
         cons[lane] = 0;
         done[lane] = in_range ? 0u : 1u;
     }
     __syncthreads();
 
-    if (warp == 1) {
+    if (!consumer) {
         // ---------------- producer ----------------
-        unsigned long long p = 0;  // draws produced (prod/cons hold its low 32 bits; differences wrap)
+        const int q = 0;
+        unsigned rounds = 0;  // rounds done by this producer (its counter; differences wrap)
         for (;;) {
             const bool act = ld_acquire(done + lane) == 0u;
             if (!__any_sync(0xffffffffu, act)) break;
+            const unsigned long long p = ((unsigned long long)rounds * NP + q) * PW;  // first draw of the round
             const unsigned c = ld_acquire(cons + lane);
-            const bool room = act && ((unsigned)p + 4u - c <= (unsigned)K);
+            const bool room = act && ((unsigned)p + (unsigned)PW - c <= (unsigned)K);
             if (__any_sync(0xffffffffu, room)) {
-                DrawPipe<4> pipe;
-                double E4[4], U4[4];
+                DrawPipe<PW> pipe;
+                double Ew[PW], Uw[PW];
                 pipe.start(gk, p);
 #pragma unroll
-                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.seed, E4, U4);
+                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.seed, Ew, Uw);
                 if (room) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) {
+                    for (int i = 0; i < PW; ++i) {
                         const int slot = (int)((p + i) & (K - 1));
-                        ringE[slot * 32 + lane] = E4[i];
-                        ringU[slot * 32 + lane] = U4[i];
+                        ringE[slot * 32 + lane] = Ew[i];
+                        ringU[slot * 32 + lane] = Uw[i];
                     }
-                    p += 4;
-                    st_release(prod + lane, (unsigned)p);
+                    ++rounds;
+                    st_release(prod + q * 32 + lane, rounds);
                 }
             } else {
                 __nanosleep(100);
@@ -125,20 +160,44 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
         const Gather<S, M> gt(tt);
         FastChain<S, M> fc;
+        fc.rates(tt, c);
         fc.load(tt, x);
 
         int stage_n = 0;  // staged records (warp-uniform)
+        unsigned long long avail = 0;  // draws of this trajectory known to be published
         double t = 0.0, t_next = 0.0, t_next2 = rp.dt;  // t_next = j*dt, t_next2 = (j+1)*dt
         long long j = 0, firings = 0;
         unsigned long long n = 0;
         int status = 0;
         bool live = in_range;
+        // optional cycle accounting of the consumer (RunParams.prof, debug):
+        // [0] waiting for draws, [1] fast batch, [2] records, [3] exact path,
+        // [4] batches, [5] total
+        unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+        const bool prof = rp.prof != nullptr;
+        long long c0 = prof ? clock64() : 0, c1 = 0;
+        const long long c_start = c0;
         while (__any_sync(0xffffffffu, live)) {
-            // draws n .. n+B-1 of every live lane must be published
-            for (;;) {
-                const bool short_ = live && ((int)(ld_acquire(prod + lane) - (unsigned)(n + B)) < 0);
-                if (!__any_sync(0xffffffffu, short_)) break;
-                __nanosleep(20);
+            // draws n .. n+B-1 of every live lane must be published; `avail`
+            // caches the last acquired bound, so the counters are re-read
+            // only when a lane runs past it
+            if (__any_sync(0xffffffffu, live && avail < n + B)) {
+                for (;;) {
+                    // producer q's first missing round is q + NP * prod_q; all
+                    // draws below (q + NP prod_q) PW of every producer are in.
+                    // Counters are 32-bit: distances to n are taken mod 2^32
+                    // (a producer is never more than K draws ahead of n)
+                    unsigned gap = 0xffffffffu;
+#pragma unroll
+                    for (int q = 0; q < NP; ++q) {
+                        const unsigned pq = ld_acquire(prod + q * 32 + lane);
+                        const unsigned gq = (pq * (unsigned)NP + (unsigned)q) * (unsigned)PW - (unsigned)n;
+                        gap = gq < gap ? gq : gap;
+                    }
+                    avail = n + gap;
+                    if (!__any_sync(0xffffffffu, live && avail < n + B)) break;
+                    __nanosleep(20);
+                }
             }
             double Eb[B], Ub[B];
 #pragma unroll
@@ -148,6 +207,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
                 Ub[k] = ringU[slot * 32 + lane];
             }
 
+            if (prof) { c1 = clock64(); pc[0] += c1 - c0; c0 = c1; pc[4] += 1; }
             // ---- fast batch (speculative, as ssa_thread_kernel); one firing
             // per batch may also cross a single sample time that is not the
             // last: it commits, and its record (pre-event state xrec, sample
@@ -195,6 +255,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
             // written 32 at a time, one per lane: the fire-and-forget limb
             // atomics of a record then run with the whole warp active instead
             // of one lane at a time.
+            if (prof) { c1 = clock64(); pc[1] += c1 - c0; c0 = c1; }
             const unsigned rmask = __ballot_sync(0xffffffffu, rec);
             if (rmask) {
                 if (rec) {
@@ -218,6 +279,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
                 }
             }
 
+            if (prof) { c1 = clock64(); pc[2] += c1 - c0; c0 = c1; }
             // ---- rare: roll back, one exact iteration ----
             if (__any_sync(0xffffffffu, bad != 0u)) {
                 double E = Eb[0], u2 = Ub[0];
@@ -273,10 +335,15 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
                 }
                 if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
             }
+            if (prof) { c1 = clock64(); pc[3] += c1 - c0; c0 = c1; }
             // release consumed slots (the slot reads above are ordered before it)
-            st_release(cons + lane, (unsigned)n);
-            if (in_range && !live) st_release(done + lane, 1u);
+            st_relaxed(cons + lane, (unsigned)n);
+            if (in_range && !live) st_relaxed(done + lane, 1u);
             asm volatile("bar.warp.sync -1;" ::: "memory");
+        }
+        if (prof && lane == 0) {
+            pc[5] = clock64() - c_start;
+            for (int i = 0; i < 6; ++i) atomicAdd(rp.prof + i, pc[i]);
         }
         __syncwarp();
         if (lane < stage_n)  // drain the staged records
@@ -292,7 +359,7 @@ __global__ void __launch_bounds__(64, 1) ssa_thread_ws_kernel(const RunParams rp
         const long long n16 = stats_bytes / 16;
         uint4 *dst = (uint4 *)((unsigned char *)rp.parts + cta * stats_bytes);
         const uint4 *src = (const uint4 *)smem;
-        for (long long i = threadIdx.x; i < n16; i += 64) dst[i] = src[i];
+        for (long long i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
     }
 }
 

@@ -1,0 +1,20 @@
+# Round evidence: GPU tests, smoke, bench lines (all configs), the ncu launch
+# list of the default bench command, and one ncu --set full capture of the
+# SSA kernel at each config's bench workload (for `traffic` and counters).
+set -x
+OUT=gpurun_out/${TAG:-final}
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/gpu.txt
+timeout 1200 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; echo bench=$?
+for c in C1 C2 C3 C4 C5; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo $c=$?; done
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo ref=$?
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_plain.json 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_ncu.log 2>&1; echo launches=$?
+for c in ${FULLCASES:-C2 C1 C3}; do
+  python tools/run_case.py --config $c > $OUT/case_$c.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:ssa_ -c 1 -o $OUT/full_$c \
+      python tools/run_case.py --config $c > $OUT/ncu_$c.log 2>&1; echo full_$c=$?
+done

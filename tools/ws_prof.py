@@ -1,0 +1,30 @@
+"""Cycle accounting of the warp-specialised consumer (debug hook CWC_PROF_PTR).
+
+    python tools/ws_prof.py --config C2 [--t-end 2]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import workloads as wl  # noqa: E402
+from paper_1010_2438_b200 import cwc  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2")
+ap.add_argument("--t-end", type=float, default=None)
+a = ap.parse_args()
+desc, sweep, cfg = wl.config(a.config)
+if a.t_end:
+    cfg["t_end"] = a.t_end
+model = cwc.cwc_model_create(desc)
+buf = torch.zeros(8, dtype=torch.int64, device="cuda")
+os.environ["CWC_PROF_PTR"] = str(buf.data_ptr())
+out = cwc.simulate(model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep)
+torch.cuda.synchronize()
+v = buf.cpu().tolist()
+nb = max(v[4], 1)
+print("warps*batches %d  cycles/batch: wait %.0f fast %.0f records %.0f exact %.0f  | total/batch %.0f" % (
+    nb, v[0] / nb, v[1] / nb, v[2] / nb, v[3] / nb, v[5] / nb))
