@@ -214,6 +214,11 @@ def run_ours(args):
     avg_nu = float(np.mean(np.diff(flat["nu_ptr"]))) if M else 0.0
     avg_dep = float(np.mean(np.diff(flat["dep_ptr"]))) if M else 0.0
     path = "warp" if info.path == cwc.CWC_PATH_WARP else "thread"
+    # the kernel the library's automatic choice launches (cwc_api.cpp plan_run):
+    # thread path -> warp-specialised kernel; warp path -> two trajectories per
+    # warp while ceil(M/16) <= 16
+    kernel_name = ("ssa_thread_ws_kernel" if path == "thread"
+                   else ("ssa_warp2_kernel" if (M + 15) // 16 <= 16 else "ssa_warp_kernel"))
 
     R = cfg["n_replicas"]
     P = len(sweep["values"]) if sweep else 1
@@ -317,8 +322,8 @@ def run_ours(args):
     achieved = ops * fired / (k_ms / 1e3)
     roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
                 "frac": achieved / peak_ops,
-                "traffic": _ncu_traffic(args.config, "ssa_thread" if path == "thread" else "ssa_warp_kernel"),
-                "ops_per_firing": ops, "kernel": "ssa_%s_kernel" % path, "kernel_ms": k_ms,
+                "traffic": _ncu_traffic(args.config, kernel_name),
+                "ops_per_firing": ops, "kernel": kernel_name, "kernel_ms": k_ms,
                 "peak_source": "issue peak = %d SMs x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
                 % (props.multi_processor_count, f_max / 1e6)}
 

@@ -56,6 +56,7 @@ struct cwc_model_s {
     std::vector<int32_t> nu_ptr, nu_cell, nu_delta;
     std::vector<int32_t> dep_ptr, dep;
     std::vector<int2> dep_slot;   // warp path: (m, slot | owner << 24) per dependency entry
+    std::vector<int2> dep_slot16; // the same for 16-lane segments
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
     int max_deps = 0;
@@ -234,6 +235,14 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
         const int r = m->dep[q], l = r / m->wt.B, k = r - l * m->wt.B;
         m->dep_slot[q] = make_int2(r, (l * m->wt.Bp + k) | (l << 24));
     }
+    // 16-lane segment layout (two trajectories per warp, ssa_warp2.cu)
+    m->wt.B16 = std::max(1, (m->M + 15) / 16);
+    m->wt.Bp16 = m->wt.B16 | 1;
+    m->dep_slot16.resize(m->dep.size());
+    for (size_t q = 0; q < m->dep.size(); ++q) {
+        const int r = m->dep[q], l = r / m->wt.B16, k = r - l * m->wt.B16;
+        m->dep_slot16[q] = make_int2(r, (l * m->wt.Bp16 + k) | (l << 24));
+    }
 
     // thread path tables
     bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
@@ -301,7 +310,7 @@ cwc_status upload(cwc_model_s *m) {
     std::vector<int2> nu2(m->nu_cell.size());
     for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
     const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
-                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_op = push_bytes(blob, m->obs_ptr),
+                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_op = push_bytes(blob, m->obs_ptr),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
     cudaError_t e = cudaGetDevice(&m->device);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaGetDevice");
@@ -317,6 +326,7 @@ cwc_status upload(cwc_model_s *m) {
     w.nu = (const int2 *)(b + o_nu);
     w.dep_ptr = (const int32_t *)(b + o_dp);
     w.dep = (const int2 *)(b + o_dep);
+    w.dep16 = (const int2 *)(b + o_dep16);
     w.obs_ptr = (const int32_t *)(b + o_op);
     w.obs_cells = (const int32_t *)(b + o_oc);
     w.init = (const int32_t *)(b + o_init);
@@ -338,6 +348,7 @@ struct Plan {
     // stats
     int stats_smem = 0;
     int ws = 0;
+    int seg2 = 0;  // warp path: two trajectories per warp
     StatLayout st{};
     int64_t cells_per_part = 0;
     int n_parts = 1;
@@ -461,7 +472,13 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         int W = bt ? std::min(bt / 32, 4) : 4;  // ssa_warp_kernel is built for <= 128 threads
         if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
         pl.warps_per_block = W;
-        const size_t per_warp = warp_smem_per_warp(w);
+        // two trajectories per warp (16-lane segments) when a segment's chunks
+        // stay short (M <= 256); the one-trajectory kernel writes traces
+        const bool tracing = opts && opts->n_trace > 0;
+        bool seg2 = !tracing && w.B16 <= 16;
+        if (const char *e = env("CWC_WARP_SEG")) seg2 = !tracing && w.B16 <= 16 && std::atoi(e) == 16;
+        pl.seg2 = seg2 ? 1 : 0;
+        const size_t per_warp = seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w);
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t stats = (size_t)stat_bytes(lay_s, cells);
@@ -654,7 +671,8 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         e = launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_thread launch");
     } else {
-        e = launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
+        e = pl.seg2 ? launch_ssa_warp2(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
+                    : launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_warp launch");
     }
     if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_end");

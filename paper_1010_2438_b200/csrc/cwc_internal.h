@@ -131,12 +131,14 @@ struct ThreadTables {
 // free).
 struct WarpTables {
     int32_t n_cells, M, O, B;     // B = reactions per lane chunk = ceil(M / 32)
-    int32_t Bp, pad_[3];          // chunk stride (odd)
+    int32_t Bp;                   // chunk stride (odd)
+    int32_t B16, Bp16, pad_;      // the same for 16-lane segments (ssa_warp2.cu)
     const ReactionDesc *rx;       // [M]
     const int32_t *nu_ptr;        // [M+1]
     const int2 *nu;               // (cell, delta)
     const int32_t *dep_ptr;       // [M+1]
     const int2 *dep;              // (m, slot | owner lane << 24) of every m in D(mu)
+    const int2 *dep16;            // the same slots for the 16-lane segment layout
     const int32_t *obs_ptr;       // [O+1]
     const int32_t *obs_cells;
     const int32_t *init;          // [n_cells]
@@ -152,6 +154,9 @@ int thread_pad_reactions(int M);
 cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                             size_t smem_bytes, cudaStream_t stream);
 size_t warp_smem_per_warp(const WarpTables &wt);
+cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+                             size_t smem_bytes, cudaStream_t stream);
+size_t warp2_smem_per_warp(const WarpTables &wt);
 
 cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,
                                 cudaStream_t stream);

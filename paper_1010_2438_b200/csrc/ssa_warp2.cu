@@ -1,0 +1,296 @@
+// ssa_warp2.cu -- two trajectories per warp (half-warp segments), for the
+// warp path's medium networks (M <= 256: C4).
+//
+// Same method, tables and result as ssa_warp_kernel (ssa_warp.cu), with the
+// 32 lanes split into two 16-lane segments that each run their own
+// trajectory.  The warp path is issue-bound (C4: ~400 warp instructions per
+// firing at ~80 % issue utilisation), and most of its instructions --
+// shuffles of the prefix scan, the division, ballots, loop control -- do the
+// same work whatever the lane count; with two segments every such
+// instruction advances two trajectories.  Lane l of segment s owns the chunk
+// of reactions [l*B16, (l+1)*B16), B16 = ceil(M/16) <= 16, stored at slots
+// l*Bp16 + k of the segment's shared memory (Bp16 = B16 | 1), with the
+// dependency slots precomputed for this layout (WarpTables.dep16).
+//
+// Every warp-wide intrinsic runs convergently with the full mask; segmented
+// behaviour comes from width-16 shuffles and from splitting ballots by
+// segment.  Side effects of a segment without a trajectory (all trajectories
+// taken) are predicated off.  Rare per-segment work (sample records, end of
+// horizon, stall, overflow, fetching the next trajectory) runs in divergent
+// branches that contain no warp-wide intrinsics, or convergently with the
+// other segment's results discarded.
+#include <cuda_runtime.h>
+
+#include "cwc_internal.h"
+#include "device_common.cuh"
+
+namespace cwc {
+
+namespace {
+
+constexpr unsigned kAll = 0xffffffffu;
+
+__device__ __forceinline__ double prop16(const WarpTables &wt, const int *xs, const double *rates, int m) {
+    const int4 d = __ldg(reinterpret_cast<const int4 *>(wt.rx) + m);
+    return __dmul_rn(__ldg(rates + m), combos(xs[d.x], xs[d.y], d.z & 1, d.z >> 1));
+}
+
+// Inclusive scan within each 16-lane segment over lanes [0, w) of the
+// segment (w a power of two <= 16, warp-uniform).
+__device__ __forceinline__ double seg_scan(double v, int sl, int w) {
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        if (d < w) {
+            const double y = __shfl_up_sync(kAll, v, d, 16);
+            if (sl >= d) v = __dadd_rn(y, v);
+        }
+    }
+    return v;
+}
+
+template <int BMAX>
+__device__ __forceinline__ double chunk_sum16(const double *ch, int B) {
+    double s = ch[0];
+#pragma unroll
+    for (int k = 1; k < BMAX; ++k)
+        if (k < B) s = __dadd_rn(s, ch[k]);
+    return s;
+}
+
+}  // namespace
+
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp, const WarpTables wt,
+                                                              long long stats_smem_bytes, int per_seg_bytes,
+                                                              int x_bytes) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int seg = lane >> 4, sl = lane & 15, sb = seg << 4;
+    const int B = wt.B16, Bp = wt.Bp16;
+    int scan_w = 1;  // in-chunk scan width: next power of two >= B (<= 16)
+    while (scan_w < B) scan_w <<= 1;
+    const int O = wt.O;
+    const int M = wt.M;
+    const long long J = rp.J, J1 = J + 1;
+
+    StatAcc acc;
+    if (rp.stats_smem) {
+        acc = stat_view(smem, rp.cells_per_part, rp.st);
+        uint4 *z = (uint4 *)smem;
+        for (long long i = threadIdx.x; i < stats_smem_bytes / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    } else {
+        acc = stat_view((unsigned char *)rp.parts + (long long)(blockIdx.x % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
+                        rp.cells_per_part, rp.st);
+    }
+    int *xs = (int *)(smem + stats_smem_bytes + (long long)(wib * 2 + seg) * per_seg_bytes);
+    double *as = (double *)((unsigned char *)xs + x_bytes);
+    __shared__ unsigned int cta_traj;  // trajectories taken by this CTA (shared-memory part capacity)
+    if (threadIdx.x == 0) cta_traj = 0;
+    __syncthreads();
+
+    // per-segment trajectory state (uniform over the segment's 16 lanes)
+    bool active = false, exhausted = false;
+    long long g = 0, cell_base = 0;
+    const double *rates = rp.rates;
+    uint64_t gk = 0;
+    double t = 0.0, t_next = 0.0, a0 = 0.0, incl = 0.0, excl = 0.0, part = 0.0;
+    long long j = 0, firings = 0;
+    unsigned long long n = 0, n_base = 0;
+    double E0 = 0.0, U0 = 0.0, E1 = 0.0, U1 = 0.0;  // draws n_base + sl and n_base + 16 + sl
+
+    auto record = [&](long long jj) {
+        for (int o = sl; o < O; o += 16) {
+            long long v = 0;
+            for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xs[__ldg(wt.obs_cells + q)];
+            stat_record(acc, cell_base + jj * O + o, v);
+            if (rp.out_traj) rp.out_traj[(g * J1 + jj) * O + o] = v;
+        }
+    };
+    auto finish = [&](int status) {  // the segment's trajectory ended
+        if (sl == 0) {
+            if (rp.out_firings) rp.out_firings[g] = firings;
+            if (rp.out_status) rp.out_status[g] = status;
+        }
+        active = false;
+    };
+
+    for (;;) {
+        // ---- segments without a trajectory take the next one ----
+        const bool need = !active && !exhausted;
+        if (__any_sync(kAll, need)) {
+            unsigned long long gg = ~0ull;
+            if (need && sl == 0) {
+                // a shared-memory part holds <= kSmemPartMaxTraj trajectories
+                if (!rp.stats_smem || atomicAdd(&cta_traj, 1u) < (unsigned)kSmemPartMaxTraj)
+                    gg = atomicAdd(rp.next_traj, 1ull);
+            }
+            gg = __shfl_sync(kAll, gg, sb);
+            const bool got = need && gg < (unsigned long long)rp.G;
+            if (need && !got) exhausted = true;
+            if (got) {
+                g = (long long)gg;
+                const long long p = g / rp.R;
+                rates = rp.rates + p * M;
+                cell_base = p * J1 * O;
+                gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);
+                for (int c = sl; c < wt.n_cells; c += 16) xs[c] = __ldg(wt.init + c);
+                if (sl == 0) xs[wt.n_cells] = 1;
+            }
+            __syncwarp();
+            double pt = 0.0;
+            for (int k = 0; k < B; ++k) {
+                const int m = sl * B + k;
+                const double a = (got && m < M) ? prop16(wt, xs, rates, m) : 0.0;
+                if (got) as[sl * Bp + k] = a;
+                pt = (k == 0) ? a : __dadd_rn(pt, a);
+            }
+            const double in = seg_scan(pt, sl, 16);
+            const double a0n = __shfl_sync(kAll, in, sb + 15);
+            const double exn = __shfl_up_sync(kAll, in, 1, 16);
+            if (got) {
+                part = pt;
+                incl = in;
+                a0 = a0n;
+                excl = (sl == 0) ? 0.0 : exn;
+                t = 0.0;
+                t_next = 0.0;
+                j = 0;
+                firings = 0;
+                n = 0;
+                n_base = 0;
+                block_to_draws(philox_block(rp.seed, gk, (uint64_t)sl), E0, U0);
+                block_to_draws(philox_block(rp.seed, gk, (uint64_t)(16 + sl)), E1, U1);
+                active = true;
+            }
+            __syncwarp();
+        }
+        if (!__any_sync(kAll, active)) break;
+
+        // ---- one firing of each active segment ----
+        const bool refill = active && (n - n_base == 32);
+        if (__any_sync(kAll, refill)) {
+            if (refill) {
+                n_base = n;
+                block_to_draws(philox_block(rp.seed, gk, n_base + sl), E0, U0);
+                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), E1, U1);
+            }
+            __syncwarp();
+        }
+        const int i = (int)(n - n_base);  // segment-uniform
+        const double E = __shfl_sync(kAll, (i < 16) ? E0 : E1, sb + (i & 15));
+        const double u2 = __shfl_sync(kAll, (i < 16) ? U0 : U1, sb + (i & 15));
+        const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
+        const double tn = __dadd_rn(t, tau);
+        bool fire = active;
+        const bool cross = active && !(tn < t_next);
+        if (__any_sync(kAll, cross)) {
+            if (cross) {  // divergent: no warp-wide intrinsics inside
+                if (a0 == 0.0) {  // stall
+                    for (; j <= J; ++j) record(j);
+                    finish(CWC_TRAJ_STALLED);
+                    fire = false;
+                } else {
+                    while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                        record(j);
+                        ++j;
+                    }
+                    if (j > J) {  // horizon reached: drawn, not applied
+                        finish(CWC_TRAJ_DONE);
+                        fire = false;
+                    } else {
+                        t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+
+        // selection: chunk L by ballot over the segment's lane prefixes, then
+        // mu inside chunk L by a segmented shuffle scan of its entries
+        const double target = __dmul_rn(u2, a0);
+        const unsigned hitsL = (__ballot_sync(kAll, incl > target) >> sb) & 0xffffu;
+        const int L = (hitsL ? __ffs(hitsL) : 1) - 1;
+        const double carry = __shfl_sync(kAll, excl, sb + L);
+        const double av = (sl < B) ? as[L * Bp + sl] : 0.0;
+        const double cum = __dadd_rn(carry, seg_scan(av, sl, scan_w));
+        const unsigned hit = (__ballot_sync(kAll, sl < B && target < cum) >> sb) & 0xffffu;
+        const unsigned pos = (__ballot_sync(kAll, av > 0.0) >> sb) & 0xffffu;
+        // the chunk's scanned sums may round below the lane prefix: take its
+        // last positive entry
+        const int mu = L * B + (hit ? __ffs(hit) - 1 : (pos ? 31 - __clz(pos) : 0));
+
+        // update: one lane per changed cell
+        const int nb = fire ? __ldg(wt.nu_ptr + mu) : 0, ne = fire ? __ldg(wt.nu_ptr + mu + 1) : 0;
+        int2 e = make_int2(0, 0);
+        long long nv = 0;
+        if (sl < ne - nb) {
+            e = __ldg(wt.nu + nb + sl);
+            nv = (long long)xs[e.x] + e.y;
+        }
+        const bool ovf = ((__ballot_sync(kAll, nv > 0x7fffffffll) >> sb) & 0xffffu) != 0u;
+        if (__any_sync(kAll, ovf)) {
+            if (ovf) {  // a count would leave int32: freeze + fill
+                for (; j <= J; ++j) record(j);
+                finish(CWC_TRAJ_OVERFLOW);
+                fire = false;
+            }
+            __syncwarp();
+        }
+        if (fire && sl < ne - nb) xs[e.x] = (int)nv;
+        __syncwarp();
+
+        // dependency-graph update: recompute a_m for m in D(mu) only
+        unsigned dirty = 0;
+        if (fire) {
+            const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
+            for (int q = db + sl; q < de; q += 16) {
+                const int2 d = __ldg(wt.dep16 + q);
+                as[d.y & 0xffffff] = prop16(wt, xs, rates, d.x);
+                dirty |= 1u << (sb + (d.y >> 24));
+            }
+        }
+        dirty = __reduce_or_sync(kAll, dirty);
+        __syncwarp();
+        if ((dirty >> lane) & 1u) part = chunk_sum16<16>(as + sl * Bp, B);
+        incl = seg_scan(part, sl, 16);
+        a0 = __shfl_sync(kAll, incl, sb + 15);
+        excl = __shfl_up_sync(kAll, incl, 1, 16);
+        if (sl == 0) excl = 0.0;
+        if (fire) {
+            t = tn;
+            ++firings;
+            ++n;
+        }
+        asm volatile("bar.warp.sync -1;" ::: "memory");  // keep the warp converged
+    }
+
+    if (rp.stats_smem) {
+        __syncthreads();
+        const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
+        uint4 *dst = (uint4 *)((unsigned char *)rp.parts + (long long)blockIdx.x * stat_bytes(rp.st, rp.cells_per_part));
+        const uint4 *src = (const uint4 *)smem;
+        for (long long q = threadIdx.x; q < n16; q += blockDim.x) dst[q] = src[q];
+    }
+}
+
+static inline int align16b(long long v) { return (int)((v + 15) & ~15ll); }
+
+size_t warp2_smem_per_warp(const WarpTables &wt) {
+    return 2 * ((size_t)align16b(4ll * (wt.n_cells + 1)) + (size_t)8 * 16 * wt.Bp16);
+}
+
+cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+                             size_t smem_bytes, cudaStream_t stream) {
+    const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
+    const int x_bytes = align16b(4ll * (wt.n_cells + 1));
+    const int per_seg = (int)(warp2_smem_per_warp(wt) / 2);
+    const bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
+    auto k = small ? ssa_warp2_kernel<8> : ssa_warp2_kernel<6>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+    k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_seg, x_bytes);
+    return cudaGetLastError();
+}
+
+}  // namespace cwc
