@@ -21,6 +21,8 @@
 // other segment's results discarded.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "cwc_internal.h"
 #include "device_common.cuh"
 
@@ -285,7 +287,8 @@ cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int bloc
     const long long stats_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
     const int x_bytes = align16b(4ll * (wt.n_cells + 1));
     const int per_seg = (int)(warp2_smem_per_warp(wt) / 2);
-    const bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
+    bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
+    if (const char *e = std::getenv("CWC_WARP2_MINB")) small = std::atoi(e) == 8 && small;  // experiment switch
     auto k = small ? ssa_warp2_kernel<8> : ssa_warp2_kernel<6>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;

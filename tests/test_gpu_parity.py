@@ -110,15 +110,28 @@ SMALL = [
      dict(t_end=0.5, sample_dt=0.05, n_replicas=70, seed=2)),
     ("rnd24", lambda: (w.random_network_model(seed=5, n_species=8, n_reactions=24), None),
      dict(t_end=0.2, sample_dt=0.02, n_replicas=45, seed=3)),
+    # warp path with B > 16 reactions per lane (sub-chunk sums): M = 525
+    ("cwc130", lambda: (w.small_cwc_model(130, 2), None), dict(t_end=0.5, sample_dt=0.05, n_replicas=40, seed=4)),
 ]
 
 
+KERNELS = [("thread", cwc.CWC_PATH_THREAD, {}),                     # warp-specialised thread kernel
+           ("thread1", cwc.CWC_PATH_THREAD, {"block_threads": 64}),  # single-warp batched thread kernel
+           ("warp", cwc.CWC_PATH_WARP, {}),                           # two trajectories per warp (M <= 256)
+           ("warp32", cwc.CWC_PATH_WARP, {"CWC_WARP_SEG": "32"})]     # one trajectory per warp
+
+
 @pytest.mark.parametrize("name,make,cfg", SMALL, ids=[s[0] for s in SMALL])
-@pytest.mark.parametrize("path", [cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP])
-def test_small_parity_full_oracle(name, make, cfg, path):
+@pytest.mark.parametrize("kname,path,kw", KERNELS, ids=[k[0] for k in KERNELS])
+def test_small_parity_full_oracle(name, make, cfg, kname, path, kw, monkeypatch):
+    kw = dict(kw)
+    if name == "cwc130" and path == cwc.CWC_PATH_THREAD:
+        pytest.skip("396 cells: warp path only")
+    for k in [k for k in kw if k.startswith("CWC_")]:
+        monkeypatch.setenv(k, kw.pop(k))
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
-    gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path)
+    gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path, **kw)
     P = gpu["n_points"]
     G = P * cfg["n_replicas"]
     same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, list(range(G)), path, path == cwc.CWC_PATH_WARP)
@@ -231,3 +244,45 @@ def test_full_config_sampled_parity(name, stride):
     assert np.allclose(a.mean(axis=0), b.mean(axis=0), rtol=1e-9, atol=0)
     if len(idx) > 1:
         assert np.allclose(a.var(axis=0, ddof=1), b.var(axis=0, ddof=1), rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_sharded_run_equals_unsharded(name):
+    """replicas split over calls (as over GPUs: replica_offset /
+    replicas_total) reproduce the unsharded trajectories; the exact integer
+    moments of the shards sum to the unsharded moments bit for bit."""
+    desc, sweep, _ = w.config(name)
+    cfg = dict(t_end=0.3 if name == "C2" else 0.05, sample_dt=0.01, n_replicas=96, seed=5)
+    model = cwc.cwc_model_create(desc)
+    full = _gpu(model, cfg, sweep)
+    parts = []
+    for off, R in ((0, 40), (40, 56)):
+        c = dict(cfg, n_replicas=R)
+        parts.append(_gpu(model, c, sweep, replica_offset=off, replicas_total=96))
+    assert torch.equal(torch.cat([p["firings"] for p in parts]), full["firings"])
+    assert torch.equal(parts[0]["count"] + parts[1]["count"], full["count"])
+    assert torch.equal(parts[0]["sum"] + parts[1]["sum"], full["sum"])
+    lo = parts[0]["sumsq"][..., 0].view(torch.int64) + parts[1]["sumsq"][..., 0].view(torch.int64)
+    assert torch.equal(lo, full["sumsq"][..., 0].view(torch.int64))  # no carry at these sizes
+
+
+def test_host_output_api_equals_device_output():
+    """cwc_simulate_host (host buffers, H2D/D2H inside the call) returns the
+    same statistics as cwc_simulate with device buffers."""
+    desc, sweep, _ = w.config("C3")
+    sweep = w.mm_sweep(4, 4)
+    cfg = dict(t_end=10.0, sample_dt=0.5, n_replicas=24, seed=3)
+    model = cwc.cwc_model_create(desc)
+    dev = _gpu(model, cfg, sweep)
+    P, J1, O = dev["count"].shape
+    hc = torch.empty(P * J1 * O, dtype=torch.int64, pin_memory=True)
+    hs = torch.empty_like(hc)
+    hq = torch.empty((P * J1 * O, 2), dtype=torch.int64, pin_memory=True)
+    ws = torch.empty(cwc.cwc_simulate_host_workspace_size(model, cfg["n_replicas"], sweep, cfg["t_end"],
+                                                         cfg["sample_dt"]), dtype=torch.uint8, device="cuda")
+    cwc.cwc_simulate_host(model, cfg["n_replicas"], sweep, cfg["t_end"], cfg["sample_dt"], cfg["seed"],
+                          torch.cuda.current_stream().cuda_stream, (hc, hs, hq), ws)
+    torch.cuda.synchronize()
+    assert torch.equal(hc.view(P, J1, O), dev["count"].cpu())
+    assert torch.equal(hs.view(P, J1, O), dev["sum"].cpu())
+    assert torch.equal(hq.view(P, J1, O, 2), dev["sumsq"].cpu())
