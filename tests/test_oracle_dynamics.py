@@ -129,11 +129,13 @@ def _linear_compartment_model():
     }
 
 
-def test_first_order_network_mean_matches_linear_ode():
-    d = _linear_compartment_model()
-    S, C = 2, 4
+def _linear_mean_ode(d):
+    """The test's own reading of the mass-action mean ODE of a model whose
+    rules all have order <= 1: dE[x]/dt = A E[x] + b (each rule applied in
+    every context of its label, and for every matching child)."""
+    S = int(d["n_species"])
+    C = len(d["parent"])
     nc = S * C
-    # the test's own reading of the mass-action mean ODE: dE[x]/dt = A E[x] + b
     A = np.zeros((nc, nc))
     b = np.zeros(nc)
     for r in d["rules"]:
@@ -148,24 +150,62 @@ def test_first_order_network_mean_matches_linear_ode():
                     nu[cell(wh, s)] += m
                 src = None
                 for (wh, s, m) in r["reactants"]:
+                    assert m == 1 and src is None, "order <= 1 only"
                     nu[cell(wh, s)] -= m
                     src = cell(wh, s)
                 if src is None:
                     b += r["rate"] * nu
                 else:
                     A[:, src] += r["rate"] * nu
+    return A, b
+
+
+def _check_linear_mean(d, n, t_end, dt, seed, samples, cells=None):
+    A, b = _linear_mean_ode(d)
+    nc = A.shape[0]
     aug = np.zeros((nc + 1, nc + 1))
     aug[:nc, :nc] = A
     aug[:nc, nc] = b
-    n = 3000
-    res = oracle.simulate(d, n, 4.0, 1.0, seed=2)
-    x0 = np.array(d["init"] + [1], dtype=float)
-    for j in (1, 2, 4):
-        m = (expm(aug * j) @ x0)[:nc]
+    res = oracle.simulate(d, n, t_end, dt, seed=seed)
+    x0 = np.array(list(d["init"]) + [1], dtype=float)
+    # observables are sums of cells: map the cell means through obs_of_cell
+    O = int(d["n_obs"])
+    Mo = np.zeros((O, nc))
+    for cidx, o in enumerate(d["obs_of_cell"]):
+        if o >= 0:
+            Mo[o, cidx] = 1.0
+    for j in samples:
+        m = Mo @ (expm(aug * (j * dt)) @ x0)[:nc]
         vals = res["traj"][:, j, :].astype(float)
-        se = vals.std(axis=0, ddof=1) / math.sqrt(n)
-        z = (vals.mean(axis=0) - m) / np.maximum(se, 1e-9)
+        # standard error, floored at one event in n trajectories (observables
+        # with very small rates may see no event at all in the sample)
+        se = np.maximum(vals.std(axis=0, ddof=1), 1.0) / math.sqrt(n)
+        z = (vals.mean(axis=0) - m) / se
         assert np.abs(z).max() < Z, (j, z)
+
+
+def test_first_order_network_mean_matches_linear_ode():
+    _check_linear_mean(_linear_compartment_model(), 3000, 4.0, 1.0, 2, (1, 2, 4))
+
+
+def test_c5_structure_linearised_mean_matches_linear_ode():
+    """The C5 CWC model (33 compartments, transport through child patterns)
+    with its dimerisation rules removed is first order: its mean obeys the
+    linear ODE exactly.  Pins the oracle's flattening of the real C5 tree
+    (1172 -> 1044 flat reactions), rates and per-type observables."""
+    d = dict(w.config("C5")[0])
+    d["rules"] = [r for r in d["rules"] if sum(m for (_, _, m) in r["reactants"]) <= 1]
+    assert len(d["rules"]) == 56 - 8
+    _check_linear_mean(d, 160, 0.2, 0.05, 3, (1, 2, 4))
+
+
+def test_c4_first_order_subnetwork_mean_matches_linear_ode():
+    """The C4 random network restricted to its order-0/1 reactions: mean vs the
+    linear ODE (pins propensities k*x and k for the generated rules)."""
+    d = dict(w.config("C4")[0])
+    d["rules"] = [r for r in d["rules"] if sum(m for (_, _, m) in r["reactants"]) <= 1]
+    assert 100 < len(d["rules"]) < 256
+    _check_linear_mean(d, 300, 0.2, 0.05, 4, (1, 2, 4))
 
 
 def test_mm_conservation_every_sample():
