@@ -25,6 +25,10 @@
 #pragma once
 #include "ssa_thread_impl.cuh"
 
+#ifndef CWC_WS_MINB
+#define CWC_WS_MINB 6  // CTAs per SM the register budget must allow (<= 170 registers; 1, 8 measured slower)
+#endif
+
 namespace cwc {
 
 
@@ -49,7 +53,7 @@ __device__ __forceinline__ void st_relaxed(unsigned *p, unsigned v) {
 }
 
 template <int S, int M>
-__global__ void __launch_bounds__(64 * kWsGroups, 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(64 * kWsGroups, CWC_WS_MINB) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
     // consumer batch B; one producer warp per group computes rounds of PW
     // draws (round r = draws [r PW, r PW + PW) of each of its trajectories)
     constexpr int B = ThreadBatch<M>::B;
