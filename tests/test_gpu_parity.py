@@ -110,7 +110,10 @@ SMALL = [
      dict(t_end=0.5, sample_dt=0.05, n_replicas=70, seed=2)),
     ("rnd24", lambda: (w.random_network_model(seed=5, n_species=8, n_reactions=24), None),
      dict(t_end=0.2, sample_dt=0.02, n_replicas=45, seed=3)),
-    # warp path with B > 16 reactions per lane (sub-chunk sums): M = 525
+    # n-species Lotka-Volterra family (NEXT-2): 4 species (both paths), 16 (warp path)
+    ("lv4", lambda: (w.lotka_volterra_chain(4), None), dict(t_end=0.3, sample_dt=0.01, n_replicas=70, seed=6)),
+    ("lv16", lambda: (w.lotka_volterra_chain(16), None), dict(t_end=0.1, sample_dt=0.01, n_replicas=40, seed=7)),
+    # warp path with B > 16 reactions per lane (one-trajectory kernel): M = 525
     ("cwc130", lambda: (w.small_cwc_model(130, 2), None), dict(t_end=0.5, sample_dt=0.05, n_replicas=40, seed=4)),
 ]
 
@@ -125,8 +128,8 @@ KERNELS = [("thread", cwc.CWC_PATH_THREAD, {}),                     # warp-speci
 @pytest.mark.parametrize("kname,path,kw", KERNELS, ids=[k[0] for k in KERNELS])
 def test_small_parity_full_oracle(name, make, cfg, kname, path, kw, monkeypatch):
     kw = dict(kw)
-    if name == "cwc130" and path == cwc.CWC_PATH_THREAD:
-        pytest.skip("396 cells: warp path only")
+    if name in ("cwc130", "lv16") and path == cwc.CWC_PATH_THREAD:
+        pytest.skip("more than 8 cells: warp path only")
     for k in [k for k in kw if k.startswith("CWC_")]:
         monkeypatch.setenv(k, kw.pop(k))
     desc, sweep = make()

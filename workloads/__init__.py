@@ -26,6 +26,7 @@ from .models import (  # noqa: F401
     dimerisation_model,
     immigration_death_model,
     isomerisation_model,
+    lotka_volterra_chain,
     lotka_volterra_model,
     michaelis_menten_model,
     mm_sweep,

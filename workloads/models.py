@@ -95,6 +95,19 @@ def lotka_volterra_model(k1=10.0, k2=0.01, k3=10.0, x0=1000, y0=1000):
     )
 
 
+def lotka_volterra_chain(n, k1=10.0, k2=0.01, k3=10.0, x0=1000):
+    """n-species Lotka-Volterra family (the workload of
+    the paper's only numeric table, fig:simd:speedup P:687-706, whose
+    parameters are not stated).  Reading: a predation chain
+    X1 -> 2 X1 (k1 X1), Xi + Xi+1 -> 2 Xi+1 (k2 Xi Xi+1, i = 1..n-1),
+    Xn -> 0 (k3 Xn); all Xi(0) = x0.  n = 2 is configs[1] (C2)."""
+    rules = [_rule(0, [(0, 0, 1)], [(0, 0, 2)], k1)]
+    for i in range(n - 1):
+        rules.append(_rule(0, [(0, i, 1), (0, i + 1, 1)], [(0, i + 1, 2)], k2))
+    rules.append(_rule(0, [(0, n - 1, 1)], [], k3))
+    return _flat_model("lotka_volterra_%d" % n, ["X%d" % (i + 1) for i in range(n)], rules, [x0] * n)
+
+
 def michaelis_menten_model(kf=1e-3, kr=1.0, kcat=0.1, e0=200, s0=1000):
     """E + S -> ES (kf), ES -> E + S (kr), ES -> E + P (kcat) -- configs[2]."""
     return _flat_model(
