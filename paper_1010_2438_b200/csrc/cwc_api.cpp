@@ -278,13 +278,13 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
                     if (m->nu_cell[q] == cell) dlt = m->nu_delta[q];
                 return dlt;
             };
-            uint64_t op = 0;
-            for (int r2 = 0; r2 < M && r2 < 4; ++r2) {
-                const int ia = tt.ia[r2], ib = tt.ib[r2];
-                op |= (uint64_t)(uint8_t)(int8_t)(ia >= 0 ? delta_of(ia) : 0) << (16 * r2);
-                op |= (uint64_t)(uint8_t)(int8_t)(ib >= 0 ? delta_of(ib) : 0) << (16 * r2 + 8);
+            uint64_t op[kOpWords] = {};
+            for (int r2 = 0; r2 < M && r2 < 4 * kOpWords; ++r2) {
+                const int ia = tt.ia[r2], ib = tt.ib[r2], wd = r2 >> 2, sh = 16 * (r2 & 3);
+                op[wd] |= (uint64_t)(uint8_t)(int8_t)(ia >= 0 ? delta_of(ia) : 0) << sh;
+                op[wd] |= (uint64_t)(uint8_t)(int8_t)(ib >= 0 ? delta_of(ib) : 0) << (sh + 8);
             }
-            tt.op_pack[k] = op;
+            for (int wd = 0; wd < kOpWords; ++wd) tt.op_pack[k][wd] = op[wd];
         }
         for (int c = 0; c < kThreadMaxCells; ++c) {
             tt.obs_of[c] = c < ncell ? m->obs_of_cell[c] : -1;

@@ -14,6 +14,7 @@ namespace cwc {
 constexpr int kThreadMaxCells = 8;
 constexpr int kThreadMaxReactions = 32;
 constexpr int kThreadMaxObs = 8;
+constexpr int kOpWords = 4;  // operand-state chain for M <= 16
 
 // Reaction encoding shared by both kernels (built by the host compiler):
 // h = xa * (xb - sub) >> shr with xa = x[ia], xb = x[ib] and index
@@ -116,10 +117,11 @@ struct ThreadTables {
     int32_t ia[kThreadMaxReactions], ib[kThreadMaxReactions];
     int32_t sub[kThreadMaxReactions], shr[kThreadMaxReactions];
     uint64_t nu_pack[kThreadMaxReactions];   // int8 delta per cell
-    // M <= 4: int8 delta of every reaction operand (byte 2m: x[ia_m], byte
-    // 2m+1: x[ib_m]; 0 for an absent reactant) -- the kernel then keeps the
-    // operands themselves as state instead of gathering them from x
-    uint64_t op_pack[kThreadMaxReactions];
+    // M <= 4 * kOpWords: int8 delta of every reaction operand (reaction m:
+    // bytes 2(m mod 4) and 2(m mod 4)+1 of word m / 4 = x[ia_m], x[ib_m]; 0
+    // for an absent reactant) -- the kernel then keeps the operands
+    // themselves as state instead of gathering them from x
+    uint64_t op_pack[kThreadMaxReactions][kOpWords];
     int32_t obs_of[kThreadMaxCells];
     int32_t init[kThreadMaxCells];
 };

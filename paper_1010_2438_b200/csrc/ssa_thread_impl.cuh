@@ -129,12 +129,13 @@ __device__ __forceinline__ bool apply_nu(const int (&x)[S], unsigned long long n
 // One speculative firing of the fast batch: propensities, a0, tau and the
 // selection, update applied at once; returns whether the firing was "plain"
 // (fast division valid -- a0 > 0 and in range --, no sample crossed, no count
-// left int32).  For M <= 4 the reaction operands x[ia_m], x[ib_m] are kept as
-// state and updated through op_pack (one compare chain selects both packed
-// deltas), so the serial chain never gathers from x.
+// left int32).  For M <= 16 the reaction operands x[ia_m], x[ib_m] are kept as
+// state and updated through op_pack (one compare chain selects the packed
+// deltas of cells and operands), so the serial chain never gathers from x.
 template <int S, int M>
 struct FastChain {
-    static constexpr bool OPND = (M <= 4);
+    static constexpr bool OPND = (M <= 4 * kOpWords);
+    static constexpr int NW = OPND ? (M + 3) / 4 : 1;  // operand delta words in use
     int A[M], Bo[M];
     // k_m * 2^-shr_m (exact scaling): then a_m = k_m' * RN(x_a (x_b - sub)),
     // which equals k_m * RN(x_a (x_b - sub) / 2^shr) bit for bit (halving
@@ -180,12 +181,17 @@ struct FastChain {
         const double a0 = cum[M - 1];
         const double tn = __dadd_rn(t, div_fast(E, a0));
         const double target = __dmul_rn(U, a0);
-        unsigned long long nu = tt.nu_pack[0], op = tt.op_pack[0];
+        unsigned long long nu = tt.nu_pack[0], op[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) op[w] = tt.op_pack[0][w];
 #pragma unroll
         for (int m = 0; m + 1 < M; ++m) {
             const bool past = cum[m] <= target;
             nu = past ? tt.nu_pack[m + 1] : nu;
-            if constexpr (OPND) op = past ? tt.op_pack[m + 1] : op;
+            if constexpr (OPND) {
+#pragma unroll
+                for (int w = 0; w < NW; ++w) op[w] = past ? tt.op_pack[m + 1][w] : op[w];
+            }
         }
         int xn[S];
         const bool wrapped = apply_nu(x, nu, xn);
@@ -198,8 +204,9 @@ struct FastChain {
         if constexpr (OPND) {
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                A[m] += (int)(signed char)(unsigned char)(op >> (16 * m));
-                Bo[m] += (int)(signed char)(unsigned char)(op >> (16 * m + 8));
+                const unsigned long long w = op[m >> 2];
+                A[m] += (int)(signed char)(unsigned char)(w >> (16 * (m & 3)));
+                Bo[m] += (int)(signed char)(unsigned char)(w >> (16 * (m & 3) + 8));
             }
         }
         return ok;

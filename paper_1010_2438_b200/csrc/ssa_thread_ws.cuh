@@ -26,7 +26,8 @@
 #include "ssa_thread_impl.cuh"
 
 #ifndef CWC_WS_MINB
-#define CWC_WS_MINB 6  // CTAs per SM the register budget must allow (<= 170 registers; 1, 8 measured slower)
+#define CWC_WS_MINB 6  // CTAs per SM the register budget must allow for small models (S*M <= 12:
+                       // <= 170 registers; 1 and 8 measured slower); larger models get the full budget
 #endif
 
 namespace cwc {
@@ -53,7 +54,7 @@ __device__ __forceinline__ void st_relaxed(unsigned *p, unsigned v) {
 }
 
 template <int S, int M>
-__global__ void __launch_bounds__(64 * kWsGroups, CWC_WS_MINB) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12) ? CWC_WS_MINB : 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
     // consumer batch B; one producer warp per group computes rounds of PW
     // draws (round r = draws [r PW, r PW + PW) of each of its trajectories)
     constexpr int B = ThreadBatch<M>::B;
