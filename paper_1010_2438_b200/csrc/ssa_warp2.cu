@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     }
     int *xs = (int *)(smem + stats_smem_bytes + (long long)(wib * 2 + seg) * per_seg_bytes);
     double *as = (double *)((unsigned char *)xs + x_bytes);
+    double2 *dr = (double2 *)(as + 16 * Bp);  // [32] the segment's draws (E, u2) of firings n_base ..
     __shared__ unsigned int cta_traj;  // trajectories taken by this CTA (shared-memory part capacity)
     if (threadIdx.x == 0) cta_traj = 0;
     __syncthreads();
@@ -99,7 +100,6 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     double t = 0.0, t_next = 0.0, a0 = 0.0, incl = 0.0, excl = 0.0, part = 0.0;
     long long j = 0, firings = 0;
     unsigned long long n = 0, n_base = 0;
-    double E0 = 0.0, U0 = 0.0, E1 = 0.0, U1 = 0.0;  // draws n_base + sl and n_base + 16 + sl
 
     auto record = [&](long long jj) {
         for (int o = sl; o < O; o += 16) {
@@ -161,8 +161,11 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                 firings = 0;
                 n = 0;
                 n_base = 0;
-                block_to_draws(philox_block(rp.seed, gk, (uint64_t)sl), E0, U0);
-                block_to_draws(philox_block(rp.seed, gk, (uint64_t)(16 + sl)), E1, U1);
+                double e0, u0, e1, u1;
+                block_to_draws(philox_block(rp.seed, gk, (uint64_t)sl), e0, u0);
+                block_to_draws(philox_block(rp.seed, gk, (uint64_t)(16 + sl)), e1, u1);
+                dr[sl] = make_double2(e0, u0);
+                dr[16 + sl] = make_double2(e1, u1);
                 active = true;
             }
             __syncwarp();
@@ -174,14 +177,17 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         if (__any_sync(kAll, refill)) {
             if (refill) {
                 n_base = n;
-                block_to_draws(philox_block(rp.seed, gk, n_base + sl), E0, U0);
-                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), E1, U1);
+                double e0, u0, e1, u1;
+                block_to_draws(philox_block(rp.seed, gk, n_base + sl), e0, u0);
+                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), e1, u1);
+                dr[sl] = make_double2(e0, u0);
+                dr[16 + sl] = make_double2(e1, u1);
             }
             __syncwarp();
         }
         const int i = (int)(n - n_base);  // segment-uniform
-        const double E = __shfl_sync(kAll, (i < 16) ? E0 : E1, sb + (i & 15));
-        const double u2 = __shfl_sync(kAll, (i < 16) ? U0 : U1, sb + (i & 15));
+        const double2 d2 = dr[i & 31];      // broadcast read (all lanes of the segment, one address)
+        const double E = d2.x, u2 = d2.y;
         const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
         const double tn = __dadd_rn(t, tau);
         bool fire = active;
@@ -278,8 +284,8 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
 
 static inline int align16b(long long v) { return (int)((v + 15) & ~15ll); }
 
-size_t warp2_smem_per_warp(const WarpTables &wt) {
-    return 2 * ((size_t)align16b(4ll * (wt.n_cells + 1)) + (size_t)8 * 16 * wt.Bp16);
+size_t warp2_smem_per_warp(const WarpTables &wt) {  // per segment: x, propensities, 32 draws
+    return 2 * ((size_t)align16b(4ll * (wt.n_cells + 1)) + (size_t)8 * 16 * wt.Bp16 + (size_t)16 * 32);
 }
 
 cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
