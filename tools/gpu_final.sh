@@ -13,7 +13,7 @@ timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_r
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_plain.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_ncu.log 2>&1; echo launches=$?
-for c in ${FULLCASES:-C2 C1 C3}; do
+for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do
   python tools/run_case.py --config $c > $OUT/case_$c.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:ssa_ -c 1 -o $OUT/full_$c \
       python tools/run_case.py --config $c > $OUT/ncu_$c.log 2>&1; echo full_$c=$?
