@@ -215,7 +215,28 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             int mu = -1;
             unsigned pos_any = 0;
             int pos_base = 0;
-            for (int k0 = 0; k0 < B; k0 += 32) {
+            if (B > 32 && B <= 64) {
+                // one pass for chunks of 33..64 entries: lane l takes entries
+                // 2l and 2l+1 (left to right), then the pair sums are scanned
+                const int k = 2 * lane;
+                const double a1 = (k < B) ? as[L * Bp + k] : 0.0;
+                const double a2 = (k + 1 < B) ? as[L * Bp + k + 1] : 0.0;
+                const double incl2 = __dadd_rn(carry, warp_incl_scan(__dadd_rn(a1, a2), lane));
+                double ex2 = __shfl_up_sync(kFull, incl2, 1);
+                if (lane == 0) ex2 = carry;
+                const double c1 = __dadd_rn(ex2, a1);
+                const unsigned h1 = __ballot_sync(kFull, k < B && target < c1);
+                const unsigned h2 = __ballot_sync(kFull, k + 1 < B && target < incl2);
+                const unsigned p1 = __ballot_sync(kFull, a1 > 0.0), p2 = __ballot_sync(kFull, a2 > 0.0);
+                if (h1 | h2) {
+                    const int l1 = h1 ? __ffs(h1) - 1 : 64, l2 = h2 ? __ffs(h2) - 1 : 64;
+                    mu = L * B + ((l1 <= l2) ? 2 * l1 : 2 * l2 + 1);
+                } else {  // rounding: the last positive entry of the chunk
+                    const int q1 = p1 ? 2 * (31 - __clz(p1)) : -1, q2 = p2 ? 2 * (31 - __clz(p2)) + 1 : -1;
+                    mu = L * B + (q1 > q2 ? q1 : q2);
+                }
+            }
+            for (int k0 = 0; mu < 0 && k0 < B; k0 += 32) {
                 const int k = k0 + lane;
                 const double a = (k < B) ? as[L * Bp + k] : 0.0;
                 const double c = __dadd_rn(carry, warp_incl_scan_w(a, lane, scan_w));
@@ -233,7 +254,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             }
             // the chunk's scanned sums may round below the lane prefix: take
             // its last positive entry
-            if (mu < 0) mu = L * B + pos_base + 31 - __clz(pos_any);
+            if (mu < 0) mu = L * B + pos_base + 31 - __clz(pos_any);  // (B <= 32 or B > 64)
             trace_rec(n, a0, tau, tn, mu);
 
             // Update: one lane per changed cell; distinct cells.
@@ -306,6 +327,7 @@ cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int block
         constexpr bool T = decltype(tr)::value;
         if (wt.B <= 8) return small ? ssa_warp_kernel<T, 8, 8> : ssa_warp_kernel<T, 6, 8>;
         if (wt.B <= 16) return small ? ssa_warp_kernel<T, 8, 16> : ssa_warp_kernel<T, 6, 16>;
+        if (wt.B <= 40) return small ? ssa_warp_kernel<T, 8, 40> : ssa_warp_kernel<T, 6, 40>;
         return small ? ssa_warp_kernel<T, 8, 0> : ssa_warp_kernel<T, 6, 0>;
     };
     auto k = (rp.n_trace > 0) ? pick(std::true_type{}) : pick(std::false_type{});

@@ -115,6 +115,8 @@ SMALL = [
     ("lv16", lambda: (w.lotka_volterra_chain(16), None), dict(t_end=0.1, sample_dt=0.01, n_replicas=40, seed=7)),
     # warp path with B > 16 reactions per lane (one-trajectory kernel): M = 525
     ("cwc130", lambda: (w.small_cwc_model(130, 2), None), dict(t_end=0.5, sample_dt=0.05, n_replicas=40, seed=4)),
+    # one-trajectory warp kernel with 33 reactions per lane (paired one-pass selection): M = 1045
+    ("cwc260", lambda: (w.small_cwc_model(260, 3), None), dict(t_end=0.4, sample_dt=0.05, n_replicas=40, seed=5)),
 ]
 
 
@@ -128,7 +130,7 @@ KERNELS = [("thread", cwc.CWC_PATH_THREAD, {}),                     # warp-speci
 @pytest.mark.parametrize("kname,path,kw", KERNELS, ids=[k[0] for k in KERNELS])
 def test_small_parity_full_oracle(name, make, cfg, kname, path, kw, monkeypatch):
     kw = dict(kw)
-    if name in ("cwc130", "lv16") and path == cwc.CWC_PATH_THREAD:
+    if name in ("cwc130", "cwc260", "lv16") and path == cwc.CWC_PATH_THREAD:
         pytest.skip("more than 8 cells: warp path only")
     for k in [k for k in kw if k.startswith("CWC_")]:
         monkeypatch.setenv(k, kw.pop(k))
