@@ -48,7 +48,10 @@ __host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, lo
 // trajectory and the ring + hand-off counters' shared-memory bytes per CTA
 constexpr int kWsRing = 32;
 constexpr int kWsProducers = 1;  // producer warps per group (2 measured slower on C2)
-constexpr int kWsGroups = 1;     // 32-trajectory groups (consumer + producer warp pairs) per CTA
+#ifndef CWC_WS_GROUPS
+#define CWC_WS_GROUPS 1
+#endif
+constexpr int kWsGroups = CWC_WS_GROUPS;  // 32-trajectory groups (consumer + producer warp pairs) per CTA
 constexpr int kWsStage = 64;     // staged sample records of a consumer warp
 constexpr size_t kWsGroupBytes = (size_t)2 * kWsRing * 32 * sizeof(double) +
                                  (size_t)(kWsProducers + 2) * 32 * sizeof(unsigned) +
