@@ -473,10 +473,9 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
         pl.warps_per_block = W;
         // two trajectories per warp (16-lane segments) when a segment's chunks
-        // stay short (M <= 256); the one-trajectory kernel writes traces
-        const bool tracing = opts && opts->n_trace > 0;
-        bool seg2 = !tracing && w.B16 <= 16;
-        if (const char *e = env("CWC_WARP_SEG")) seg2 = !tracing && w.B16 <= 16 && std::atoi(e) == 16;
+        // stay short (M <= 256); both kernels write traces
+        bool seg2 = w.B16 <= 16;
+        if (const char *e = env("CWC_WARP_SEG")) seg2 = w.B16 <= 16 && std::atoi(e) == 16;
         pl.seg2 = seg2 ? 1 : 0;
         const size_t per_warp = seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w);
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);

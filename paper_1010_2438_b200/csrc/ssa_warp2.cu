@@ -61,7 +61,7 @@ __device__ __forceinline__ double chunk_sum16(const double *ch, int B) {
 
 }  // namespace
 
-template <int MINB>
+template <int MINB, bool TRACE>
 __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp, const WarpTables wt,
                                                               long long stats_smem_bytes, int per_seg_bytes,
                                                               int x_bytes) {
@@ -101,6 +101,20 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     long long j = 0, firings = 0;
     unsigned long long n = 0, n_base = 0;
 
+    // divergence tracer (TRACE builds): per-firing records (n, a0, tau, t', mu)
+    // of the trajectories listed in rp.trace_g, written by the segment's lane 0
+    int tslot = -1;
+    long long tn_rec = 0;
+    auto trace_rec = [&](unsigned long long n_, double a0_, double tau, double tn, int mu) {
+        if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
+            if (sl == 0) {
+                double *r = rp.trace_buf + ((long long)tslot * rp.trace_cap + tn_rec) * 5;
+                r[0] = (double)n_; r[1] = a0_; r[2] = tau; r[3] = tn; r[4] = (double)mu;
+            }
+            ++tn_rec;
+        }
+    };
+
     auto record = [&](long long jj) {
         for (int o = sl; o < O; o += 16) {
             long long v = 0;
@@ -113,6 +127,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         if (sl == 0) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
+            if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
         }
         active = false;
     };
@@ -136,6 +151,12 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                 rates = rp.rates + p * M;
                 cell_base = p * J1 * O;
                 gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);
+                if (TRACE) {
+                    tslot = -1;
+                    tn_rec = 0;
+                    for (int q = 0; q < rp.n_trace; ++q)
+                        if (rp.trace_g[q] == g) tslot = q;
+                }
                 for (int c = sl; c < wt.n_cells; c += 16) xs[c] = __ldg(wt.init + c);
                 if (sl == 0) xs[wt.n_cells] = 1;
             }
@@ -204,6 +225,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                         ++j;
                     }
                     if (j > J) {  // horizon reached: drawn, not applied
+                        trace_rec(n, a0, tau, tn, -1);
                         finish(CWC_TRAJ_DONE);
                         fire = false;
                     } else {
@@ -227,6 +249,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         // the chunk's scanned sums may round below the lane prefix: take its
         // last positive entry
         const int mu = L * B + (hit ? __ffs(hit) - 1 : (pos ? 31 - __clz(pos) : 0));
+        if (TRACE && fire) trace_rec(n, a0, tau, tn, mu);
 
         // update: one lane per changed cell
         const int nb = fire ? __ldg(wt.nu_ptr + mu) : 0, ne = fire ? __ldg(wt.nu_ptr + mu + 1) : 0;
@@ -295,7 +318,8 @@ cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int bloc
     const int per_seg = (int)(warp2_smem_per_warp(wt) / 2);
     bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
     if (const char *e = std::getenv("CWC_WARP2_MINB")) small = std::atoi(e) == 8 && small;  // experiment switch
-    auto k = small ? ssa_warp2_kernel<8> : ssa_warp2_kernel<6>;
+    auto k = (rp.n_trace > 0) ? (small ? ssa_warp2_kernel<8, true> : ssa_warp2_kernel<6, true>)
+                              : (small ? ssa_warp2_kernel<8, false> : ssa_warp2_kernel<6, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_seg, x_bytes);

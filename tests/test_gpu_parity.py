@@ -208,6 +208,20 @@ def test_finalize_matches_oracle_moments():
         assert np.all(np.abs(g - wv) <= 1e-9 * np.maximum(np.abs(g), np.abs(wv)))
 
 
+@pytest.mark.parametrize("seg", ["16", "32"])
+def test_trace_warp_paths_against_oracle(seg, monkeypatch):
+    """The warp kernels' per-firing traces (n, a0, tau, t', mu) against the
+    oracle's: identical or differing only by the classified ulp-level
+    reasons (sum order of a0 / the chunk prefixes, log ulp), never BUG."""
+    monkeypatch.setenv("CWC_WARP_SEG", seg)
+    desc = w.random_network_model(seed=5, n_species=8, n_reactions=24)
+    cfg = dict(t_end=0.2, sample_dt=0.02, n_replicas=20, seed=3)
+    model = cwc.cwc_model_create(desc)
+    rep = trace_mismatches(model, desc, None, cfg, [0, 7, 19], True, cwc.CWC_PATH_WARP)
+    for g, cat, idx, detail in rep:
+        assert cat in ("identical-trace", "log-ulp", "a0-sum-order", "select-order"), (g, cat, idx, detail)
+
+
 def test_trace_equals_oracle_trace_thread_path():
     desc, _, _ = w.config("C2")
     cfg = dict(t_end=0.5, sample_dt=0.01, n_replicas=64, seed=1)
