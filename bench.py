@@ -217,7 +217,10 @@ def run_ours(args):
     # the kernel the library's automatic choice launches (cwc_api.cpp plan_run):
     # thread path -> warp-specialised kernel; warp path -> two trajectories per
     # warp while ceil(M/16) <= 16
-    kernel_name = ("ssa_thread_ws_kernel" if path == "thread"
+    G_all = (len(sweep["values"]) if sweep else 1) * cfg["n_replicas"]
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    kernel_name = (("ssa_thread_ws_kernel" if (G_all + 31) // 32 <= 8 * n_sm else "ssa_thread_kernel")
+                   if path == "thread"
                    else ("ssa_warp2_kernel" if (M + 15) // 16 <= 16 else "ssa_warp_kernel"))
 
     R = cfg["n_replicas"]

@@ -425,8 +425,12 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories;
         // ssa_thread_ws.cuh); the single-warp kernel serves traced runs and
         // explicit block sizes
+        // warp-specialised producer/consumer CTAs while trajectory warps are
+        // scarce (<= 2 per SM sub-partition: C1, C2); with more (C3) the
+        // single-warp kernel, whose warps carry their own draws, uses every
+        // sub-partition (measured: C3 11.2 vs 11.9 ms, C2 6.4e10 vs 6.9e10)
         const bool tracing = opts && opts->n_trace > 0;
-        bool ws = !tracing && !bt;
+        bool ws = !tracing && !bt && (pl.G + 31) / 32 <= 2ll * 4 * nsm;
         if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
         if (ws) T = 32 * kWsGroups;
         pl.ws = ws ? 1 : 0;
@@ -444,7 +448,9 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int64_t cells = stat_cells_round(np_max * J1 * O);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t smem = (size_t)stat_bytes(lay_s, cells);
-        const size_t extra = ws ? kWsRingBytes : 0;
+        // beyond the statistics part: the draw ring + staging of the
+        // warp-specialised CTA, or the record staging of each warp
+        const size_t extra = ws ? kWsRingBytes : (size_t)(T / 32) * kStageLL * sizeof(long long);
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
         bool use_smem = smem + extra <= smem_cap &&
                         (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;

@@ -43,6 +43,13 @@
 #include "cwc_internal.h"
 #include "device_common.cuh"
 
+#ifndef CWC_T_MAXT  // single-warp thread kernel: CTA size bound and CTAs per SM (register budget)
+#define CWC_T_MAXT 256
+#endif
+#ifndef CWC_T_MINB
+#define CWC_T_MINB 1
+#endif
+
 namespace cwc {
 
 template <int S>
@@ -232,7 +239,7 @@ struct ThreadBatch {
 };
 
 template <int S, int M, bool TRACE>
-__global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
     constexpr int B = ThreadBatch<M>::B;
     extern __shared__ __align__(16) unsigned char smem[];
     const long long T = blockDim.x;
@@ -243,6 +250,13 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
     const int O = tt.O;
     const long long J = rp.J;
     const long long J1 = J + 1;
+
+    // staged sample records of this warp (after the statistics part)
+    const long long stats_part_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
+    long long *st_cell = (long long *)(smem + stats_part_bytes) + (long long)(threadIdx.x >> 5) * kStageLL;
+    long long *st_v = st_cell + kWsStage;  // [kWsStage][kThreadMaxObs]
+    const int lane = threadIdx.x & 31;
+    int stage_n = 0;  // warp-uniform
 
     StatAcc acc;
     long long p_base = 0;
@@ -293,6 +307,7 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
         fc.load(tt, x);
 
         double t = 0.0, t_next = 0.0;  // t_next = j * dt: sample 0 is crossed by the first firing
+        double t_next2 = rp.dt;        // (j + 1) * dt
         long long j = 0, firings = 0;
         unsigned long long n = 0;
         int status = 0;
@@ -314,6 +329,12 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
             int xsnap[B][S];
             double tsnap[B];
             unsigned bad = 0;  // bit k: firing k of the batch is not plain
+            // one firing per batch may cross a single sample time that is not
+            // the last: it commits, its record (pre-event state) follows the batch
+            bool rec = false;
+            int krec = B;
+            long long jrec = 0;
+            int xrec[S];
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
@@ -322,16 +343,57 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
+                bool cross1;
+                const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
+                const bool take = cross1 && !rec && (j < J);
+                if (take) {
+                    rec = true;
+                    krec = k;
+                    jrec = j;
+#pragma unroll
+                    for (int s = 0; s < S; ++s) xrec[s] = xsnap[k][s];
+                    j += 1;
+                    t_next = t_next2;
+                    t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+                }
                 // TRACE builds take every firing through the exact path below
                 // (it writes the trace)
-                const bool ok = fc.step(tt, gt, c, x, t, Eb[k], Ub[k], t_next) && !TRACE;
-                bad |= ok ? 0u : (1u << k);
+                bad |= (!TRACE && (plain || take)) ? 0u : (1u << k);
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
+            if (rec && krec >= used) {  // the crossing firing was rolled back
+                rec = false;
+                j = jrec;
+                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+            }
             if (live) {
                 n += (unsigned long long)used;
                 firings += used;
+            }
+            // records staged in shared memory, written 32 at a time (one per lane)
+            const unsigned rmask = __ballot_sync(0xffffffffu, rec);
+            if (rmask) {
+                if (rec) {
+                    const int slot = stage_n + __popc(rmask & ((1u << lane) - 1u));
+                    st_cell[slot] = cell_base + jrec * O;
+                    for (int o = 0; o < O; ++o) {
+                        long long v = 0;
+#pragma unroll
+                        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)xrec[s] : 0ll;
+                        st_v[slot * kThreadMaxObs + o] = v;
+                        if (rp.out_traj) rp.out_traj[(g * J1 + jrec) * O + o] = v;
+                    }
+                }
+                stage_n += __popc(rmask);
+                if (stage_n >= 32) {
+                    __syncwarp();
+                    const int e = stage_n - 32 + lane;
+                    for (int o = 0; o < O; ++o) stat_record(acc, st_cell[e] + o, st_v[e * kThreadMaxObs + o]);
+                    stage_n -= 32;
+                    __syncwarp();
+                }
             }
 
             // ---- rare: roll back to the first non-plain firing, run ONE exact
@@ -371,6 +433,7 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
                             live = false;
                         } else {
                             t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                            t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
                             int mu;
                             const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
                             int xn[S];
@@ -426,6 +489,9 @@ __global__ void __launch_bounds__(256, 1) ssa_thread_kernel(const RunParams rp, 
             // __syncwarp() is elided by the compiler here)
             asm volatile("bar.warp.sync -1;" ::: "memory");
         }
+        __syncwarp();
+        if (lane < stage_n)  // drain the staged records
+            for (int o = 0; o < O; ++o) stat_record(acc, st_cell[lane] + o, st_v[lane * kThreadMaxObs + o]);
         if (in_range) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
