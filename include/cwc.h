@@ -46,8 +46,9 @@ typedef enum {
     CWC_ERR_NOMEM = -4        /* device or host allocation failed */
 } cwc_status;
 
-/* Per-trajectory outcome codes written to cwc_sim_opts.out_status. */
-enum { CWC_TRAJ_DONE = 0, CWC_TRAJ_STALLED = 1, CWC_TRAJ_OVERFLOW = 2 };
+/* Per-trajectory outcome codes written to cwc_sim_opts.out_status.
+   RUNNING: suspended by a resumable run's bound (cwc_run_advance), not done. */
+enum { CWC_TRAJ_DONE = 0, CWC_TRAJ_STALLED = 1, CWC_TRAJ_OVERFLOW = 2, CWC_TRAJ_RUNNING = 3 };
 
 /* Which kernel runs the SSA loop. */
 enum { CWC_PATH_AUTO = -1, CWC_PATH_THREAD = 0, CWC_PATH_WARP = 1 };
@@ -251,6 +252,68 @@ cwc_status cwc_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t 
  * IEEE div.rn otherwise.  Must equal the IEEE quotient bit for bit.  Device
  * arrays.  Test hook. */
 cwc_status cwc_tau_div(const double *e, const double *a, int64_t count, double *q, void *cuda_stream);
+
+/*
+ * Resumable runs.  The paper's schema (ii)
+ * makes every simulation instance an object that holds its progress, so a
+ * scheduler can stop it and restart it later -- in (fixed or variable)
+ * slices, on any worker; schema (iii) reduces a running window of
+ * the trajectories while they advance almost aligned in simulated time.  Here
+ * the whole progress of trajectory g is (x, t, n, j): counts, time, applied
+ * firings n (= its Philox counter) and next sample j (j = J+1: finished).  A
+ * suspended trajectory therefore resumes bit-exactly, and a run split into
+ * any sequence of advances produces exactly the statistics, firings, status
+ * and samples of one cwc_simulate call with the same arguments.
+ *
+ * `state` is ONE caller-owned device buffer of cwc_run_state_size bytes that
+ * holds everything the run needs between calls: per-trajectory state, the
+ * live list, the per-point rates and the statistics accumulators.  The
+ * library keeps nothing between calls, so copying the buffer to host memory
+ * and back (to this or another device) is a checkpoint; the layout is
+ * private but fixed for given arguments.  Every cwc_run_* call on one state
+ * must pass the same model, n_replicas, sweep, t_end, sample_dt and
+ * (force_path, replica_offset, replicas_total) of opts; the kernel choice
+ * may differ from cwc_simulate's (the warp-specialised thread kernel is not
+ * used), the results do not.  opts->n_trace must be 0.
+ */
+cwc_status cwc_run_state_size(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                              double sample_dt, const cwc_sim_opts *opts, size_t *bytes);
+
+/* Start a run: every trajectory at (x0, t = 0, n = 0, j = 0), all live
+ * (listed longest-expected-first for sweeps), statistics zeroed.  Also stores
+ * the per-point rates (host expansion of sweep).  Asynchronous on
+ * cuda_stream.  Errors: as cwc_simulate, CWC_ERR_INVALID for a short state. */
+cwc_status cwc_run_init(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                        double sample_dt, const cwc_sim_opts *opts, void *state, size_t state_bytes,
+                        void *cuda_stream);
+
+/* Advance every live trajectory by at most `quantum` further applied firings
+ * (0 = no bound; the bound is checked once per batch / 32-draw window, so a
+ * trajectory may run a few firings past it) and at most up to sample j_stop:
+ * a trajectory suspends, before drawing into effect, once all its samples
+ * j < j_stop are recorded (j_stop = J+1, or 0, = no bound).  Then drops the
+ * finished trajectories from the live list (order kept), so the next advance
+ * launches only unfinished ones, in dense warps.  With a j_stop bound and no
+ * quantum, every live trajectory ends the call at j = j_stop: the statistics
+ * of samples < j_stop are final (the running window of schema iii).
+ * opts->out_firings / out_status receive the cumulative firings and status
+ * (CWC_TRAJ_RUNNING = suspended) of the trajectories this call ran;
+ * out_traj the samples it recorded.  *n_pending (HOST) receives the number
+ * of trajectories that still have samples below j_stop to record (with
+ * j_stop = J+1: the unfinished ones; 0 = the window, or the run, is
+ * complete); the call synchronises cuda_stream to read it (n_pending may be
+ * NULL: it still synchronises). */
+cwc_status cwc_run_advance(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                           double sample_dt, uint64_t seed, const cwc_sim_opts *opts, int64_t quantum,
+                           int64_t j_stop, void *state, size_t state_bytes, void *cuda_stream,
+                           int64_t *n_pending);
+
+/* Reduce the run's accumulators into out_stats (device, as cwc_simulate's):
+ * cells of samples every trajectory has passed are final; the others hold
+ * the partial sums so far.  Asynchronous on cuda_stream. */
+cwc_status cwc_run_stats(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                         double sample_dt, const cwc_sim_opts *opts, const void *state, size_t state_bytes,
+                         cwc_stats out_stats, void *cuda_stream);
 
 /* Thread-local message of the last failure on this thread ("" if none). */
 const char *cwc_last_error(void);

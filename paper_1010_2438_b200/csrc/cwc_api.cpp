@@ -337,6 +337,7 @@ cwc_status upload(cwc_model_s *m) {
 struct Plan {
     int path = 0;
     int64_t G = 0, R = 0;
+    int64_t n_launch = 0;  // trajectories in this launch (resumable runs: the live ones)
     int32_t P = 1, J = 0;
     int64_t n_stat_cells = 0;  // P * (J+1) * O
     // thread path
@@ -372,8 +373,11 @@ int sm_count() {
     return n > 0 ? n : 148;
 }
 
+// resumable = cwc_run_* (global statistics accumulators, no warp-specialised
+// kernel, n_launch = live trajectories of this launch; -1 = all G)
 cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt,
-                    const cwc_sim_opts *opts, bool host_stats, Plan &pl) {
+                    const cwc_sim_opts *opts, bool host_stats, Plan &pl, bool resumable = false,
+                    int64_t n_launch = -1) {
     if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
     if (!(t_end > 0.0) || !std::isfinite(t_end)) return fail(CWC_ERR_INVALID, "t_end must be finite and > 0");
     if (!(dt > 0.0) || !std::isfinite(dt)) return fail(CWC_ERR_INVALID, "sample_dt must be finite and > 0");
@@ -397,6 +401,9 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     if ((double)pl.P * (double)n_replicas >= 4294967296.0)  // statistics words take < 2^32 adds
         return fail(CWC_ERR_INVALID, "too many trajectories in one call (shard the run: replica_offset)");
     pl.G = (int64_t)pl.P * n_replicas;
+    if (resumable && opts && opts->n_trace > 0) return fail(CWC_ERR_INVALID, "resumable runs do not trace (n_trace must be 0)");
+    const int64_t NL = (n_launch < 0) ? pl.G : std::min<int64_t>(n_launch, pl.G);  // trajectories launched
+    pl.n_launch = NL;
     const int64_t J1 = (int64_t)pl.J + 1;
     const int O = m->n_obs;
     pl.n_stat_cells = (int64_t)pl.P * J1 * O;
@@ -432,10 +439,11 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const bool tracing = opts && opts->n_trace > 0;
         bool ws = !tracing && !bt && (pl.G + 31) / 32 <= 2ll * 4 * nsm;
         if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
+        if (resumable) ws = false;
         if (ws) T = 32 * kWsGroups;
         pl.ws = ws ? 1 : 0;
         pl.threads = T;
-        const int64_t blocks = (pl.G + T - 1) / T;
+        const int64_t blocks = (NL + T - 1) / T;
         if (blocks > 0x7fffffffll) return fail(CWC_ERR_INVALID, "too many trajectories for one launch");
         pl.blocks = (int)blocks;
         // points touched by one block
@@ -455,7 +463,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         bool use_smem = smem + extra <= smem_cap &&
                         (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
-        if (O == 0) use_smem = false;
+        if (O == 0 || resumable) use_smem = false;
         if (use_smem) {
             pl.stats_smem = 1;
             pl.st = lay_s;
@@ -492,7 +500,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // global-memory parts (fire-and-forget REDs to L2) are nearly free
         bool use_smem = (stats + W * per_warp) * 8 <= 200 * 1024;
         if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
-        if (O == 0) use_smem = false;
+        if (O == 0 || resumable) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
         pl.st = use_smem ? lay_s : lay_g;
         pl.cells_per_part = cells;
@@ -506,7 +514,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         per_sm = std::min(by_smem, by_threads);
         if (const char *e = env("CWC_BLOCKS_PER_SM")) per_sm = std::atoi(e);
         int64_t blocks = (int64_t)nsm * per_sm;
-        blocks = std::min<int64_t>(blocks, (pl.G + W - 1) / W);
+        blocks = std::min<int64_t>(blocks, (NL + W - 1) / W);
         pl.blocks = (int)std::max<int64_t>(1, blocks);
         pl.threads = W * 32;
         // a shared-memory part takes <= 2^16 trajectories (16-bit limbs); the
@@ -545,6 +553,77 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     return CWC_OK;
 }
 
+// per-point flat rates [P][M] (host expansion of the sweep)
+std::vector<double> expand_rates(const cwc_model_s *m, const Plan &pl, const cwc_sweep *sweep) {
+    const int M = m->M;
+    std::vector<double> rates((size_t)pl.P * std::max(M, 1), 0.0);
+    std::vector<double> rule_rates(m->rule_rate);
+    for (int p = 0; p < pl.P; ++p) {
+        if (sweep)
+            for (int i = 0; i < sweep->n_swept; ++i) rule_rates[sweep->rule[i]] = sweep->value[(size_t)p * sweep->n_swept + i];
+        for (int k = 0; k < M; ++k) rates[(size_t)p * M + k] = rule_rates[m->entry_rule[k]];
+    }
+    return rates;
+}
+
+// Expected work of each point's trajectories: the total propensity a0(x0)
+// (firings per unit time at t = 0), the longest-first dispatch key for sweeps.
+std::vector<double> point_a0(const cwc_model_s *m, const Plan &pl, const std::vector<double> &rates) {
+    const int M = m->M;
+    std::vector<double> a0p(pl.P, 0.0);
+    for (int p = 0; p < pl.P; ++p) {
+        double a0 = 0.0;
+        for (int k = 0; k < M; ++k) {
+            const ReactionDesc &r = m->rx[k];
+            const double xa = r.ia < m->n_cells ? (double)m->init[r.ia] : 1.0;
+            const double xb = r.ib < m->n_cells ? (double)m->init[r.ib] - (r.kind & 1) : 1.0;
+            a0 += rates[(size_t)p * M + k] * xa * xb / ((r.kind >> 1) ? 2.0 : 1.0);
+        }
+        a0p[p] = a0;
+    }
+    return a0p;
+}
+
+// Groups of T consecutive trajectories in longest-expected-first order.
+std::vector<int32_t> lpt_groups(const Plan &pl, const std::vector<double> &a0p, int64_t T) {
+    const int64_t n_groups = (pl.G + T - 1) / T;
+    std::vector<std::pair<double, int32_t>> w8(n_groups);
+    for (int64_t b = 0; b < n_groups; ++b) {
+        double s = 0.0;
+        const int64_t ge = std::min<int64_t>((b + 1) * T, pl.G);
+        for (int64_t gg = b * T; gg < ge; ++gg) s += a0p[gg / pl.R];
+        w8[b] = {-s, (int32_t)b};
+    }
+    std::stable_sort(w8.begin(), w8.end());
+    std::vector<int32_t> order(n_groups);
+    for (int64_t b = 0; b < n_groups; ++b) order[b] = w8[b].second;
+    return order;
+}
+
+// Sharding and optional outputs of opts (both one-shot and resumable runs).
+cwc_status apply_shard(RunParams &rp, const cwc_sim_opts *opts, int64_t n_replicas) {
+    if (!opts) return CWC_OK;
+    if (opts->replicas_total != 0) {
+        if (opts->replica_offset < 0 || opts->replicas_total < opts->replica_offset + n_replicas)
+            return fail(CWC_ERR_INVALID, "replica_offset + n_replicas must be <= replicas_total");
+        rp.R_total = opts->replicas_total;
+        rp.r_off = opts->replica_offset;
+    } else if (opts->replica_offset != 0) {
+        return fail(CWC_ERR_INVALID, "replica_offset needs replicas_total");
+    }
+    rp.out_traj = opts->out_traj;
+    rp.out_firings = opts->out_firings;
+    rp.out_status = opts->out_status;
+    return CWC_OK;
+}
+
+cudaError_t launch_ssa(const cwc_model_s *m, const Plan &pl, const RunParams &rp, cudaStream_t stream) {
+    if (pl.path == CWC_PATH_THREAD)
+        return launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
+    return pl.seg2 ? launch_ssa_warp2(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
+                   : launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
+}
+
 cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt, uint64_t seed,
                void *stream_, cwc_stats st, void *ws, size_t ws_bytes, const cwc_sim_opts *opts, bool host_stats,
                cwc_stats host_out) {
@@ -564,15 +643,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     cudaStream_t stream = (cudaStream_t)stream_;
     unsigned char *w = (unsigned char *)ws;
 
-    // per-point flat rates [P][M] (host expansion of the sweep)
-    const int M = m->M;
-    std::vector<double> rates((size_t)pl.P * std::max(M, 1), 0.0);
-    std::vector<double> rule_rates(m->rule_rate);
-    for (int p = 0; p < pl.P; ++p) {
-        if (sweep)
-            for (int i = 0; i < sweep->n_swept; ++i) rule_rates[sweep->rule[i]] = sweep->value[(size_t)p * sweep->n_swept + i];
-        for (int k = 0; k < M; ++k) rates[(size_t)p * M + k] = rule_rates[m->entry_rule[k]];
-    }
+    const std::vector<double> rates = expand_rates(m, pl, sweep);
     cudaError_t e = cudaMemcpyAsync(w + pl.off_rates, rates.data(), sizeof(double) * rates.size(), cudaMemcpyHostToDevice, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: rates upload");
 
@@ -586,6 +657,8 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.dt = dt;
     rp.seed = seed;
     rp.rates = (const double *)(w + pl.off_rates);
+    rp.n_launch = pl.G;
+    rp.j_stop = (int64_t)pl.J + 1;
     rp.parts = w + pl.off_parts;
     rp.cells_per_part = pl.cells_per_part;
     rp.st = pl.st;
@@ -596,17 +669,8 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.next_traj = (unsigned long long *)(w + pl.off_counter);
     if (const char *e = env("CWC_PROF_PTR")) rp.prof = (unsigned long long *)std::strtoull(e, nullptr, 0);  // debug hook
     if (opts) {
-        if (opts->replicas_total != 0) {
-            if (opts->replica_offset < 0 || opts->replicas_total < opts->replica_offset + n_replicas)
-                return fail(CWC_ERR_INVALID, "replica_offset + n_replicas must be <= replicas_total");
-            rp.R_total = opts->replicas_total;
-            rp.r_off = opts->replica_offset;
-        } else if (opts->replica_offset != 0) {
-            return fail(CWC_ERR_INVALID, "replica_offset needs replicas_total");
-        }
-        rp.out_traj = opts->out_traj;
-        rp.out_firings = opts->out_firings;
-        rp.out_status = opts->out_status;
+        s = apply_shard(rp, opts, n_replicas);
+        if (s != CWC_OK) return s;
         if (opts->n_trace > 0) {
             e = cudaMemcpyAsync(w + pl.off_trace, opts->trace_g, sizeof(int64_t) * opts->n_trace, cudaMemcpyHostToDevice, stream);
             if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: trace ids upload");
@@ -630,29 +694,9 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         // the total propensity a0(x0) of its trajectories' points (firings per
         // unit time at t = 0).  Trajectory ids -- hence the RNG streams and
         // every result -- are unchanged; only the start order moves.
-        std::vector<double> a0p(pl.P, 0.0);
-        for (int p = 0; p < pl.P; ++p) {
-            double a0 = 0.0;
-            for (int k = 0; k < M; ++k) {
-                const ReactionDesc &r = m->rx[k];
-                const double xa = r.ia < m->n_cells ? (double)m->init[r.ia] : 1.0;
-                const double xb = r.ib < m->n_cells ? (double)m->init[r.ib] - (r.kind & 1) : 1.0;
-                a0 += rates[(size_t)p * M + k] * xa * xb / ((r.kind >> 1) ? 2.0 : 1.0);
-            }
-            a0p[p] = a0;
-        }
         const int T = pl.ws ? 32 * kWsGroups : pl.threads;
-        std::vector<std::pair<double, int32_t>> w8(pl.blocks);
-        for (int b = 0; b < pl.blocks; ++b) {
-            double s = 0.0;
-            const int64_t ge = std::min<int64_t>((int64_t)(b + 1) * T, pl.G);
-            for (int64_t gg = (int64_t)b * T; gg < ge; ++gg) s += a0p[gg / pl.R];
-            w8[b] = {-s, b};
-        }
-        std::stable_sort(w8.begin(), w8.end());
         // pageable source: cudaMemcpyAsync has copied it when it returns
-        std::vector<int32_t> order_host(pl.blocks);
-        for (int b = 0; b < pl.blocks; ++b) order_host[b] = w8[b].second;
+        const std::vector<int32_t> order_host = lpt_groups(pl, point_a0(m, pl, rates), T);
         e = cudaMemcpyAsync(w + pl.off_order, order_host.data(), sizeof(int32_t) * pl.blocks, cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: dispatch order upload");
         rp.cta_order = (const int32_t *)(w + pl.off_order);
@@ -672,14 +716,8 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     cudaEvent_t ev0 = opts ? (cudaEvent_t)opts->ev_kernel_begin : nullptr;
     cudaEvent_t ev1 = opts ? (cudaEvent_t)opts->ev_kernel_end : nullptr;
     if (ev0 && (e = cudaEventRecord(ev0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_begin");
-    if (pl.path == CWC_PATH_THREAD) {
-        e = launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_thread launch");
-    } else {
-        e = pl.seg2 ? launch_ssa_warp2(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
-                    : launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: ssa_warp launch");
-    }
+    e = launch_ssa(m, pl, rp, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: SSA kernel launch");
     if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_end");
     cwc_stats dst = st;
     if (host_stats) {
@@ -702,9 +740,225 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     return CWC_OK;
 }
 
+// ---- resumable runs (cwc_run_*) -------------------------------------------------
+// One caller-owned device buffer: header (live count, dispatch counter,
+// compaction count), per-point rates, the global statistics part, the
+// per-trajectory state (x [G][n_cells] int32, t, n, j), two live lists
+// (current, compaction target) and the compaction's scratch.
+struct StateLayout {
+    size_t hdr = 0, rates = 0, parts = 0, x = 0, t = 0, n = 0, j = 0, live0 = 0, live1 = 0, temp = 0, temp_bytes = 0,
+           total = 0;
+};
+constexpr size_t kHdrLive = 0, kHdrCounter = 16, kHdrOut = 32, kHdrPending = 40, kHdrBytes = 256;
+
+StateLayout state_layout(const cwc_model_s *m, const Plan &pl) {
+    StateLayout l;
+    const size_t G = (size_t)pl.G;
+    size_t off = 0;
+    l.hdr = off;
+    off = align256(off + kHdrBytes);
+    l.rates = off;
+    off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
+    l.parts = off;
+    off = align256(off + (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts);
+    l.x = off;
+    off = align256(off + sizeof(int32_t) * G * (size_t)std::max(m->n_cells, 1));
+    l.t = off;
+    off = align256(off + sizeof(double) * G);
+    l.n = off;
+    off = align256(off + sizeof(int64_t) * G);
+    l.j = off;
+    off = align256(off + sizeof(int32_t) * G);
+    l.live0 = off;
+    off = align256(off + sizeof(int64_t) * G);
+    l.live1 = off;
+    off = align256(off + sizeof(int64_t) * G);
+    l.temp = off;
+    l.temp_bytes = compact_temp_bytes((long long)G);
+    off = align256(off + l.temp_bytes);
+    l.total = off;
+    return l;
+}
+
+cwc_status run_prepare(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt,
+                       const cwc_sim_opts *opts, const void *state, size_t state_bytes, Plan &pl, StateLayout &sl) {
+    if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, dt, opts, false, pl, true, -1);
+    if (s != CWC_OK) return s;
+    sl = state_layout(m, pl);
+    if (!state) return fail(CWC_ERR_INVALID, "state is NULL");
+    if (state_bytes < sl.total) return fail(CWC_ERR_INVALID, "state too small: need " + std::to_string(sl.total) + " bytes");
+    if (!m->dev.p) {
+        s = upload(m);
+        if (s != CWC_OK) return s;
+    }
+    return CWC_OK;
+}
+
+RunParams run_params(const cwc_model_s *m, const Plan &pl, const StateLayout &sl, unsigned char *st, double dt,
+                     uint64_t seed) {
+    RunParams rp{};
+    rp.G = pl.G;
+    rp.R = pl.R;
+    rp.R_total = pl.R;
+    rp.r_off = 0;
+    rp.P = pl.P;
+    rp.J = pl.J;
+    rp.dt = dt;
+    rp.seed = seed;
+    rp.rates = (const double *)(st + sl.rates);
+    rp.parts = st + sl.parts;
+    rp.st = pl.st;
+    rp.cells_per_part = pl.cells_per_part;
+    rp.stats_smem = 0;
+    rp.ws = 0;
+    rp.n_parts = pl.n_parts;
+    rp.traj_per_part = 0;
+    rp.next_traj = (unsigned long long *)(st + sl.hdr + kHdrCounter);
+    rp.n_launch = pl.n_launch;
+    rp.rs_live = (const int64_t *)(st + sl.live0);
+    rp.rs_x = (int32_t *)(st + sl.x);
+    rp.rs_t = (double *)(st + sl.t);
+    rp.rs_n = (int64_t *)(st + sl.n);
+    rp.rs_j = (int32_t *)(st + sl.j);
+    rp.quantum = 0;
+    rp.j_stop = (int64_t)pl.J + 1;
+    (void)m;
+    return rp;
+}
+
 }  // namespace
 
 extern "C" {
+
+cwc_status cwc_run_state_size(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
+                              double sample_dt, const cwc_sim_opts *opts, size_t *bytes) {
+    if (!bytes) return fail(CWC_ERR_INVALID, "bytes is NULL");
+    if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
+    Plan pl;
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl, true, -1);
+    if (s != CWC_OK) return s;
+    *bytes = state_layout(m, pl).total;
+    return CWC_OK;
+}
+
+cwc_status cwc_run_init(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                        const cwc_sim_opts *opts, void *state, size_t state_bytes, void *cuda_stream) {
+    Plan pl;
+    StateLayout sl;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl);
+    if (s != CWC_OK) return s;
+    cudaStream_t stream = (cudaStream_t)cuda_stream;
+    unsigned char *st = (unsigned char *)state;
+    const std::vector<double> rates = expand_rates(m, pl, sweep);
+    cudaError_t e = cudaMemcpyAsync(st + sl.rates, rates.data(), sizeof(double) * rates.size(), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: rates upload");
+    e = cudaMemsetAsync(st + sl.parts, 0, (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: zero accumulators");
+    // sweeps: the live list starts longest-expected-first, in groups of 32
+    // (a warp of the thread path); compaction keeps that order
+    const bool lpt = pl.P > 1;
+    e = launch_state_init(pl.G, m->n_cells, m->wt.init, (int32_t *)(st + sl.x), (double *)(st + sl.t),
+                          (int64_t *)(st + sl.n), (int32_t *)(st + sl.j), lpt ? nullptr : (int64_t *)(st + sl.live0),
+                          stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: state");
+    if (lpt) {
+        const int64_t T = 32;
+        const std::vector<int32_t> order = lpt_groups(pl, point_a0(m, pl, rates), T);
+        std::vector<int64_t> live;
+        live.reserve(pl.G);
+        for (int32_t b : order)
+            for (int64_t gg = b * T; gg < std::min<int64_t>((b + 1) * T, pl.G); ++gg) live.push_back(gg);
+        // pageable source: cudaMemcpyAsync has copied it when it returns
+        e = cudaMemcpyAsync(st + sl.live0, live.data(), sizeof(int64_t) * live.size(), cudaMemcpyHostToDevice, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: live list");
+    }
+    const int64_t hdr[2] = {pl.G, 0};
+    e = cudaMemcpyAsync(st + sl.hdr + kHdrLive, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: header");
+    return CWC_OK;
+}
+
+cwc_status cwc_run_advance(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                           uint64_t seed, const cwc_sim_opts *opts, int64_t quantum, int64_t j_stop, void *state,
+                           size_t state_bytes, void *cuda_stream, int64_t *n_pending) {
+    Plan pl0;
+    StateLayout sl;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl0, sl);
+    if (s != CWC_OK) return s;
+    if (quantum < 0) return fail(CWC_ERR_INVALID, "quantum must be >= 0");
+    if (j_stop == 0) j_stop = (int64_t)pl0.J + 1;
+    if (j_stop < 1 || j_stop > (int64_t)pl0.J + 1) return fail(CWC_ERR_INVALID, "j_stop must be in [1, J+1] (or 0)");
+    cudaStream_t stream = (cudaStream_t)cuda_stream;
+    unsigned char *st = (unsigned char *)state;
+    int64_t nl = 0;
+    cudaError_t e = cudaMemcpyAsync(&nl, st + sl.hdr + kHdrLive, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: live count");
+    if (nl < 0 || nl > pl0.G) return fail(CWC_ERR_INVALID, "state header corrupt (live count out of range)");
+    int64_t n_out = 0;
+    if (nl > 0) {
+        Plan pl;
+        s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl, true, nl);
+        if (s != CWC_OK) return s;
+        RunParams rp = run_params(m, pl, sl, st, sample_dt, seed);
+        s = apply_shard(rp, opts, n_replicas);
+        if (s != CWC_OK) return s;
+        rp.quantum = quantum;
+        rp.j_stop = j_stop;
+        e = cudaMemsetAsync(st + sl.hdr + kHdrCounter, 0, 16, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: counter");
+        cudaEvent_t ev0 = opts ? (cudaEvent_t)opts->ev_kernel_begin : nullptr;
+        cudaEvent_t ev1 = opts ? (cudaEvent_t)opts->ev_kernel_end : nullptr;
+        if (ev0 && (e = cudaEventRecord(ev0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_run_advance: ev_kernel_begin");
+        e = launch_ssa(m, pl, rp, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: SSA kernel launch");
+        if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_run_advance: ev_kernel_end");
+        // compaction: live1 = unfinished entries of live0 (order kept)
+        int64_t *cnt = (int64_t *)(st + sl.hdr + kHdrOut);
+        e = launch_compact((const int64_t *)(st + sl.live0), nl, (int64_t *)(st + sl.live1), cnt, rp.rs_j, pl.J,
+                           st + sl.temp, sl.temp_bytes, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: compaction");
+        unsigned long long *pend = (unsigned long long *)(st + sl.hdr + kHdrPending);
+        int64_t n_unfinished = 0;
+        e = cudaMemcpyAsync(&n_unfinished, cnt, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: live count");
+        if (n_unfinished > 0) {
+            e = cudaMemcpyAsync(st + sl.live0, st + sl.live1, sizeof(int64_t) * (size_t)n_unfinished, cudaMemcpyDeviceToDevice, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: live list");
+        }
+        e = cudaMemcpyAsync(st + sl.hdr + kHdrLive, cnt, sizeof(int64_t), cudaMemcpyDeviceToDevice, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: header");
+        if (n_unfinished > 0 && j_stop <= (int64_t)pl0.J) {  // pending: unfinished and below the window bound
+            e = launch_count_below((const int64_t *)(st + sl.live0), n_unfinished, rp.rs_j, (int32_t)j_stop, pend, stream);
+            unsigned long long np = 0;
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&np, pend, sizeof(np), cudaMemcpyDeviceToHost, stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: pending count");
+            n_out = (int64_t)np;
+        } else {
+            n_out = n_unfinished;
+        }
+    }
+    if (n_pending) *n_pending = n_out;
+    return CWC_OK;
+}
+
+cwc_status cwc_run_stats(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                         const cwc_sim_opts *opts, const void *state, size_t state_bytes, cwc_stats out_stats,
+                         void *cuda_stream) {
+    Plan pl;
+    StateLayout sl;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl);
+    if (s != CWC_OK) return s;
+    if (pl.n_stat_cells == 0) return CWC_OK;
+    if (!out_stats.count || !out_stats.sum || !out_stats.sumsq) return fail(CWC_ERR_INVALID, "stats pointers are NULL");
+    const RunParams rp = run_params(m, pl, sl, (unsigned char *)state, sample_dt, 0);
+    cudaError_t e = launch_stats_stage2(rp, m->n_obs, out_stats.count, out_stats.sum, out_stats.sumsq, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_stats: stage-2 launch");
+    return CWC_OK;
+}
 
 cwc_status cwc_model_create(const cwc_model_desc *desc, cwc_model *out) {
     if (!out) return fail(CWC_ERR_INVALID, "out is NULL");

@@ -113,7 +113,27 @@ struct RunParams {
     unsigned long long *next_traj;
     // debug: consumer cycle accounting of the warp-specialised kernel (NULL = off)
     unsigned long long *prof;
+    // launch slots and resumable runs (cwc_run_*).  Slot i
+    // < n_launch runs trajectory rs_live[i] (i itself when rs_live is NULL).
+    // With rs_x set, every trajectory starts from and ends by saving its state
+    // (x [G][n_cells], t, n = applied firings = Philox counter, j = next
+    // sample; j = J+1: finished) and is suspended after `quantum` further
+    // firings (0 = no bound; checked per batch / per 32-draw window) or on
+    // reaching sample j_stop (J+1 = no bound).  One-shot runs: rs_* NULL,
+    // n_launch = G, quantum = 0, j_stop = J+1.
+    int64_t n_launch;
+    const int64_t *rs_live;
+    int32_t *rs_x;
+    double *rs_t;
+    int64_t *rs_n;
+    int32_t *rs_j;
+    int64_t quantum;
+    int64_t j_stop;
 };
+
+__host__ __device__ __forceinline__ long long launch_traj(const RunParams &rp, long long slot) {
+    return rp.rs_live ? (long long)rp.rs_live[slot] : slot;
+}
 
 // Thread path tables (kernel parameter, constant bank).
 struct ThreadTables {
@@ -173,5 +193,14 @@ cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t 
 cudaError_t launch_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
                          cudaStream_t stream);
 cudaError_t launch_tau_div(const double *e, const double *a, int64_t count, double *q, cudaStream_t stream);
+
+// resume.cu: resumable runs (state initialisation, live-list compaction)
+cudaError_t launch_state_init(long long G, int n_cells, const int32_t *init, int32_t *x, double *t, int64_t *n,
+                              int32_t *j, int64_t *live, cudaStream_t stream);
+size_t compact_temp_bytes(long long G);
+cudaError_t launch_compact(const int64_t *live_in, long long n_in, int64_t *live_out, int64_t *n_out,
+                           const int32_t *j, int32_t J, void *temp, size_t temp_bytes, cudaStream_t stream);
+cudaError_t launch_count_below(const int64_t *live, long long n, const int32_t *j, int32_t j_stop,
+                               unsigned long long *out, cudaStream_t stream);
 
 }  // namespace cwc

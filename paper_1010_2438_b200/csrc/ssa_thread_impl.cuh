@@ -245,8 +245,8 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
     const long long T = blockDim.x;
     // dispatch order: CTA slot blockIdx.x runs trajectory group cta (RunParams.cta_order)
     const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
-    const long long g0 = cta * T;
-    const long long g = g0 + threadIdx.x;
+    const long long g0 = cta * T;  // first launch slot of the CTA
+    const long long slot = g0 + threadIdx.x;
     const int O = tt.O;
     const long long J = rp.J;
     const long long J1 = J + 1;
@@ -274,8 +274,9 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
 
     // Lanes past the last trajectory stay in the warp-uniform loop as idle
     // lanes (their loads use a valid trajectory id; they never record).
-    const bool in_range = g < rp.G;
-    const long long gc = in_range ? g : rp.G - 1;
+    const bool in_range = slot < rp.n_launch;
+    const long long g = launch_traj(rp, in_range ? slot : rp.n_launch - 1);  // trajectory of the lane
+    const long long gc = g;
     {
         const long long p = gc / rp.R;
         const long long cell_base = (p - p_base) * J1 * O;
@@ -295,9 +296,21 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             }
         };
 
+        // state: fresh (x0, t = 0, n = 0, j = 0) or resumed (cwc_run_advance)
         int x[S];
 #pragma unroll
-        for (int s = 0; s < S; ++s) x[s] = (s < tt.n_cells) ? tt.init[s] : 0;
+        for (int s = 0; s < S; ++s)
+            x[s] = (s < tt.n_cells) ? (rp.rs_x ? rp.rs_x[g * tt.n_cells + s] : tt.init[s]) : 0;
+        double t = 0.0;
+        long long j = 0;
+        unsigned long long n = 0;
+        if (rp.rs_x) {
+            t = rp.rs_t[g];
+            j = rp.rs_j[g];
+            n = (unsigned long long)rp.rs_n[g];
+        }
+        const long long JL = rp.j_stop - 1;  // last sample of this launch (J in one-shot runs)
+        const unsigned long long n_start = n;
         double c[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
@@ -306,16 +319,15 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         fc.rates(tt, c);
         fc.load(tt, x);
 
-        double t = 0.0, t_next = 0.0;  // t_next = j * dt: sample 0 is crossed by the first firing
-        double t_next2 = rp.dt;        // (j + 1) * dt
-        long long j = 0, firings = 0;
-        unsigned long long n = 0;
-        int status = 0;
+        double t_next = __dmul_rn(__ll2double_rn(j), rp.dt);  // j * dt (fresh: sample 0 is crossed by the first firing)
+        double t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);  // (j + 1) * dt
+        long long firings = (long long)n;
+        int status = CWC_TRAJ_DONE;
         double Eb[B], Ub[B];
 #pragma unroll
         for (int i = 0; i < B; ++i) block_to_draws(philox_block(rp.seed, gk, n + i), Eb[i], Ub[i]);
 
-        bool live = in_range;
+        bool live = in_range && j <= JL;
         while (__any_sync(0xffffffffu, live)) {
             // ---- fast batch: B firings run speculatively (every step commits
             // its update); the four phases of the next batch's draws
@@ -345,7 +357,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                 tsnap[k] = t;
                 bool cross1;
                 const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
-                const bool take = cross1 && !rec && (j < J);
+                const bool take = cross1 && !rec && (j < JL);
                 if (take) {
                     rec = true;
                     krec = k;
@@ -417,17 +429,17 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                     cumulative(tt, gt, x, c, cum);
                     const double a0 = cum[M - 1];
                     if (a0 == 0.0) {  // stall: no draw is consumed
-                        for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
+                        for (; j <= JL; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
                         status = CWC_TRAJ_STALLED;
                         live = false;
                     } else {
                         const double tau = __ddiv_rn(E, a0);
                         const double tn = __dadd_rn(t, tau);
-                        while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                        while (j <= JL && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
                             record_sample(rp, tt, acc, x, cell_base, g, j);
                             ++j;
                         }
-                        if (j > J) {  // horizon reached: drawn, not applied
+                        if (j > JL) {  // horizon (or the launch's last sample) reached: drawn, not applied
                             trace_rec(n, a0, tau, tn, -1);
                             status = CWC_TRAJ_DONE;
                             live = false;
@@ -438,7 +450,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                             const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
                             int xn[S];
                             if (apply_nu(x, nu, xn)) {  // a count would leave int32: freeze + fill
-                                for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
+                                for (; j <= JL; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
                                 status = CWC_TRAJ_OVERFLOW;
                                 live = false;
                             } else {
@@ -483,6 +495,8 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                 Eb[i] = En[i];
                 Ub[i] = Un[i];
             }
+            // resumable runs: suspend after `quantum` further firings
+            if (rp.quantum > 0 && live && n - n_start >= (unsigned long long)rp.quantum) live = false;
             // reconverge the warp explicitly: the vote at the loop head only
             // synchronises it, and a warp left split after the rare path would
             // run every later batch twice with half its lanes (a plain
@@ -493,9 +507,18 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         if (lane < stage_n)  // drain the staged records
             for (int o = 0; o < O; ++o) stat_record(acc, st_cell[lane] + o, st_v[lane * kThreadMaxObs + o]);
         if (in_range) {
+            if (j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
+            if (rp.rs_x) {
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    if (s < tt.n_cells) rp.rs_x[g * tt.n_cells + s] = x[s];
+                rp.rs_t[g] = t;
+                rp.rs_n[g] = (int64_t)n;
+                rp.rs_j[g] = (int32_t)j;
+            }
         }
     }
 
@@ -514,7 +537,7 @@ __global__ void ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt);
 template <int S, int M>
 cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, size_t smem, cudaStream_t st,
                       bool trace) {
-    const long long blocks = (rp.G + threads - 1) / threads;
+    const long long blocks = (rp.n_launch + threads - 1) / threads;
     if (rp.ws && !trace) {  // warp-specialised: 32 trajectories per 2-warp CTA (ssa_thread_ws.cuh)
         auto k = ssa_thread_ws_kernel<S, M>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

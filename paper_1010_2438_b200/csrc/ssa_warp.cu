@@ -86,7 +86,9 @@ __device__ __forceinline__ double chunk_sum(const double *ch, int B) {
 
 // MINB: CTAs per SM the register allocation must allow (8 -> 64 registers,
 // for models whose per-warp shared memory lets 8 CTAs reside; 6 -> 80).
-template <bool TRACE, int MINB, int BMAX>
+// RES: resumable runs (cwc_run_*: state load/save, launch bounds); the
+// one-shot instantiation carries none of it (measured: C5 -8 % otherwise)
+template <bool TRACE, int MINB, int BMAX, bool RES>
 __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp, const WarpTables wt, long long stats_smem_bytes,
                                                        int per_warp_bytes, int x_bytes) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
     int *xs = (int *)(smem + stats_smem_bytes + (long long)wib * per_warp_bytes);
     double *as = (double *)((unsigned char *)xs + x_bytes);
     __shared__ unsigned int cta_traj;  // trajectories taken by this CTA (shared-memory part capacity)
+    __shared__ unsigned long long q_stop[RES ? 32 : 1];  // per warp: resumable runs' firing bound
     if (threadIdx.x == 0) cta_traj = 0;
     __syncthreads();
 
@@ -122,8 +125,8 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             if (!rp.stats_smem || atomicAdd(&cta_traj, 1u) < (unsigned)kSmemPartMaxTraj) gg = atomicAdd(rp.next_traj, 1ull);
         }
         gg = __shfl_sync(kFull, gg, 0);
-        if (gg >= (unsigned long long)rp.G) break;
-        const long long g = (long long)gg;
+        if (gg >= (unsigned long long)(RES ? rp.n_launch : rp.G)) break;
+        const long long g = RES ? launch_traj(rp, (long long)gg) : (long long)gg;
         const long long p = g / rp.R;
         const double *rates = rp.rates + p * M;
         const long long cell_base = p * J1 * O;
@@ -147,8 +150,22 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             }
         };
 
-        for (int c = lane; c < wt.n_cells; c += 32) xs[c] = __ldg(wt.init + c);
+        // state: fresh (x0, t = 0, n = 0, j = 0) or resumed (cwc_run_advance)
+        for (int c = lane; c < wt.n_cells; c += 32)
+            xs[c] = RES ? rp.rs_x[g * wt.n_cells + c] : __ldg(wt.init + c);
         if (lane == 0) xs[wt.n_cells] = 1;
+        double t = 0.0;
+        long long j = 0;
+        unsigned long long n = 0;
+        if (RES) {
+            t = rp.rs_t[g];
+            j = rp.rs_j[g];
+            n = (unsigned long long)rp.rs_n[g];
+        }
+        // resumable bounds: samples j < jend in this launch (J+1 in one-shot
+        // runs); the quantum's firing bound sits in shared memory
+        const long long jend = RES ? (long long)rp.j_stop : J1;
+        if (RES && lane == 0) q_stop[wib] = rp.quantum > 0 ? n + (unsigned long long)rp.quantum : ~0ull;
         __syncwarp();
 
         double part = 0.0;
@@ -173,15 +190,20 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             }
         };
 
-        double t = 0.0, t_next = 0.0;
-        long long j = 0, firings = 0;
-        unsigned long long n = 0, n_base = 0;
+        double t_next = RES ? __dmul_rn(__ll2double_rn(j), rp.dt) : 0.0;
+        unsigned long long n_base = n;
+        long long firings = (long long)n;
         int status = CWC_TRAJ_DONE;
         double El, u2l;
-        block_to_draws(philox_block(rp.seed, gk, (uint64_t)lane), El, u2l);
+        block_to_draws(philox_block(rp.seed, gk, n_base + lane), El, u2l);
 
-        for (;;) {
+        // (a trajectory resumed at its launch's sample bound -- j_stop
+        // windows -- has nothing to do)
+        if (!RES || j < jend) for (;;) {
             if (n - n_base == 32) {
+                // resumable runs: suspend after `quantum` further firings (at a
+                // 32-draw window boundary)
+                if (RES && n >= q_stop[wib]) break;
                 n_base = n;
                 block_to_draws(philox_block(rp.seed, gk, n_base + lane), El, u2l);
             }
@@ -193,15 +215,15 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             const double tn = __dadd_rn(t, tau);
             if (!(tn < t_next)) {
                 if (a0 == 0.0) {
-                    for (; j <= J; ++j) record(j);
+                    for (; j < jend; ++j) record(j);
                     status = CWC_TRAJ_STALLED;
                     break;
                 }
-                while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                while (j < jend && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
                     record(j);
                     ++j;
                 }
-                if (j > J) {
+                if (j >= jend) {  // horizon (or the launch's last sample): drawn, not applied
                     trace_rec(n, a0, tau, tn, -1);
                     status = CWC_TRAJ_DONE;
                     break;
@@ -266,7 +288,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
                 nv = (long long)xs[e.x] + e.y;
             }
             if (__any_sync(kFull, nv > 0x7fffffffll)) {  // a count would leave int32: freeze
-                for (; j <= J; ++j) record(j);
+                for (; j < jend; ++j) record(j);
                 status = CWC_TRAJ_OVERFLOW;
                 break;
             }
@@ -294,10 +316,19 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             ++n;
             asm volatile("bar.warp.sync -1;" ::: "memory");  // keep the warp converged
         }
+        if (RES && j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
         if (lane == 0) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
+        }
+        if (RES) {
+            for (int c = lane; c < wt.n_cells; c += 32) rp.rs_x[g * wt.n_cells + c] = xs[c];
+            if (lane == 0) {
+                rp.rs_t[g] = t;
+                rp.rs_n[g] = (int64_t)n;
+                rp.rs_j[g] = (int32_t)j;
+            }
         }
         __syncwarp();
     }
@@ -323,14 +354,16 @@ cudaError_t launch_ssa_warp(const RunParams &rp, const WarpTables &wt, int block
     const int x_bytes = align16(4ll * (wt.n_cells + 1));
     const int per_warp = (int)warp_smem_per_warp(wt);
     const bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
-    auto pick = [&](auto tr) {
-        constexpr bool T = decltype(tr)::value;
-        if (wt.B <= 8) return small ? ssa_warp_kernel<T, 8, 8> : ssa_warp_kernel<T, 6, 8>;
-        if (wt.B <= 16) return small ? ssa_warp_kernel<T, 8, 16> : ssa_warp_kernel<T, 6, 16>;
-        if (wt.B <= 40) return small ? ssa_warp_kernel<T, 8, 40> : ssa_warp_kernel<T, 6, 40>;
-        return small ? ssa_warp_kernel<T, 8, 0> : ssa_warp_kernel<T, 6, 0>;
+    auto pick = [&](auto tr, auto rs) {
+        constexpr bool T = decltype(tr)::value, R = decltype(rs)::value;
+        if (wt.B <= 8) return small ? ssa_warp_kernel<T, 8, 8, R> : ssa_warp_kernel<T, 6, 8, R>;
+        if (wt.B <= 16) return small ? ssa_warp_kernel<T, 8, 16, R> : ssa_warp_kernel<T, 6, 16, R>;
+        if (wt.B <= 40) return small ? ssa_warp_kernel<T, 8, 40, R> : ssa_warp_kernel<T, 6, 40, R>;
+        return small ? ssa_warp_kernel<T, 8, 0, R> : ssa_warp_kernel<T, 6, 0, R>;
     };
-    auto k = (rp.n_trace > 0) ? pick(std::true_type{}) : pick(std::false_type{});
+    // resumable runs never trace (the planner refuses it)
+    auto k = rp.rs_x ? pick(std::false_type{}, std::true_type{})
+                     : (rp.n_trace > 0) ? pick(std::true_type{}, std::false_type{}) : pick(std::false_type{}, std::false_type{});
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, stats_bytes, per_warp, x_bytes);

@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     uint64_t gk = 0;
     double t = 0.0, t_next = 0.0, a0 = 0.0, incl = 0.0, excl = 0.0, part = 0.0;
     long long j = 0, firings = 0;
-    unsigned long long n = 0, n_base = 0;
+    unsigned long long n = 0, n_base = 0, n_start = 0;
+    const long long JL = rp.j_stop - 1;  // last sample of this launch (J in one-shot runs)
 
     // divergence tracer (TRACE builds): per-firing records (n, a0, tau, t', mu)
     // of the trajectories listed in rp.trace_g, written by the segment's lane 0
@@ -123,11 +124,20 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
             if (rp.out_traj) rp.out_traj[(g * J1 + jj) * O + o] = v;
         }
     };
-    auto finish = [&](int status) {  // the segment's trajectory ended
+    auto finish = [&](int status) {  // the segment's trajectory ended or is suspended
+        if (j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;
         if (sl == 0) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
+        }
+        if (rp.rs_x) {  // resumable runs: save (x, t, n, j)
+            for (int c = sl; c < wt.n_cells; c += 16) rp.rs_x[g * wt.n_cells + c] = xs[c];
+            if (sl == 0) {
+                rp.rs_t[g] = t;
+                rp.rs_n[g] = (int64_t)n;
+                rp.rs_j[g] = (int32_t)j;
+            }
         }
         active = false;
     };
@@ -143,10 +153,10 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                     gg = atomicAdd(rp.next_traj, 1ull);
             }
             gg = __shfl_sync(kAll, gg, sb);
-            const bool got = need && gg < (unsigned long long)rp.G;
+            const bool got = need && gg < (unsigned long long)rp.n_launch;
             if (need && !got) exhausted = true;
             if (got) {
-                g = (long long)gg;
+                g = launch_traj(rp, (long long)gg);
                 const long long p = g / rp.R;
                 rates = rp.rates + p * M;
                 cell_base = p * J1 * O;
@@ -157,7 +167,9 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                     for (int q = 0; q < rp.n_trace; ++q)
                         if (rp.trace_g[q] == g) tslot = q;
                 }
-                for (int c = sl; c < wt.n_cells; c += 16) xs[c] = __ldg(wt.init + c);
+                // state: fresh (x0, t = 0, n = 0, j = 0) or resumed (cwc_run_advance)
+                for (int c = sl; c < wt.n_cells; c += 16)
+                    xs[c] = rp.rs_x ? rp.rs_x[g * wt.n_cells + c] : __ldg(wt.init + c);
                 if (sl == 0) xs[wt.n_cells] = 1;
             }
             __syncwarp();
@@ -177,17 +189,24 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                 a0 = a0n;
                 excl = (sl == 0) ? 0.0 : exn;
                 t = 0.0;
-                t_next = 0.0;
                 j = 0;
-                firings = 0;
                 n = 0;
-                n_base = 0;
+                if (rp.rs_x) {
+                    t = rp.rs_t[g];
+                    j = rp.rs_j[g];
+                    n = (unsigned long long)rp.rs_n[g];
+                }
+                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                firings = (long long)n;
+                n_base = n;
+                n_start = n;
                 double e0, u0, e1, u1;
-                block_to_draws(philox_block(rp.seed, gk, (uint64_t)sl), e0, u0);
-                block_to_draws(philox_block(rp.seed, gk, (uint64_t)(16 + sl)), e1, u1);
+                block_to_draws(philox_block(rp.seed, gk, n_base + sl), e0, u0);
+                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), e1, u1);
                 dr[sl] = make_double2(e0, u0);
                 dr[16 + sl] = make_double2(e1, u1);
                 active = true;
+                if (j > JL) finish(CWC_TRAJ_DONE);  // resumed at its launch's sample bound
             }
             __syncwarp();
         }
@@ -196,7 +215,11 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         // ---- one firing of each active segment ----
         const bool refill = active && (n - n_base == 32);
         if (__any_sync(kAll, refill)) {
-            if (refill) {
+            // resumable runs: suspend after `quantum` further firings (at a
+            // 32-draw window boundary)
+            if (refill && rp.quantum > 0 && n - n_start >= (unsigned long long)rp.quantum) {
+                finish(CWC_TRAJ_DONE);
+            } else if (refill) {
                 n_base = n;
                 double e0, u0, e1, u1;
                 block_to_draws(philox_block(rp.seed, gk, n_base + sl), e0, u0);
@@ -216,15 +239,15 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         if (__any_sync(kAll, cross)) {
             if (cross) {  // divergent: no warp-wide intrinsics inside
                 if (a0 == 0.0) {  // stall
-                    for (; j <= J; ++j) record(j);
+                    for (; j <= JL; ++j) record(j);
                     finish(CWC_TRAJ_STALLED);
                     fire = false;
                 } else {
-                    while (j <= J && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                    while (j <= JL && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
                         record(j);
                         ++j;
                     }
-                    if (j > J) {  // horizon reached: drawn, not applied
+                    if (j > JL) {  // horizon (or the launch's last sample) reached: drawn, not applied
                         trace_rec(n, a0, tau, tn, -1);
                         finish(CWC_TRAJ_DONE);
                         fire = false;
@@ -262,7 +285,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         const bool ovf = ((__ballot_sync(kAll, nv > 0x7fffffffll) >> sb) & 0xffffu) != 0u;
         if (__any_sync(kAll, ovf)) {
             if (ovf) {  // a count would leave int32: freeze + fill
-                for (; j <= J; ++j) record(j);
+                for (; j <= JL; ++j) record(j);
                 finish(CWC_TRAJ_OVERFLOW);
                 fire = false;
             }

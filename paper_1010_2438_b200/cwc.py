@@ -19,12 +19,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcwcsim.so")
 
 CWC_OK, CWC_ERR_INVALID, CWC_ERR_UNSUPPORTED, CWC_ERR_CUDA, CWC_ERR_NOMEM = 0, -1, -2, -3, -4
-CWC_TRAJ_DONE, CWC_TRAJ_STALLED, CWC_TRAJ_OVERFLOW = 0, 1, 2
+CWC_TRAJ_DONE, CWC_TRAJ_STALLED, CWC_TRAJ_OVERFLOW, CWC_TRAJ_RUNNING = 0, 1, 2, 3
 CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
 
 EXPORTED = ["cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
             "cwc_simulate_workspace_size", "cwc_simulate", "cwc_simulate_host", "cwc_simulate_host_workspace_size",
-            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_tau_div", "cwc_last_error"]
+            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_tau_div", "cwc_run_state_size",
+            "cwc_run_init", "cwc_run_advance", "cwc_run_stats", "cwc_last_error"]
 
 P = ctypes.c_void_p
 I32 = ctypes.c_int32
@@ -90,6 +91,12 @@ def lib():
         L.cwc_philox_blocks.argtypes = [ctypes.c_uint64, P, P, I64, P, P]
         L.cwc_draws.argtypes = [ctypes.c_uint64, P, P, I64, P, P, P]
         L.cwc_tau_div.argtypes = [P, P, I64, P, P]
+        D = ctypes.c_double
+        L.cwc_run_state_size.argtypes = [P, I64, P, D, D, P, ctypes.POINTER(ctypes.c_size_t)]
+        L.cwc_run_init.argtypes = [P, I64, P, D, D, P, P, ctypes.c_size_t, P]
+        L.cwc_run_advance.argtypes = [P, I64, P, D, D, ctypes.c_uint64, P, I64, I64, P, ctypes.c_size_t, P,
+                                      ctypes.POINTER(I64)]
+        L.cwc_run_stats.argtypes = [P, I64, P, D, D, P, P, ctypes.c_size_t, cwc_stats, P]
         L.cwc_last_error.restype = ctypes.c_char_p
         L.cwc_last_error.argtypes = []
         for name in EXPORTED:
@@ -260,6 +267,48 @@ def cwc_tau_div(e, a, q, stream):
     _check(lib().cwc_tau_div(_ptr(e), _ptr(a), int(e.numel()), _ptr(q), ctypes.c_void_p(stream)))
 
 
+def _sw(sweep):
+    return _SweepArrays(sweep) if sweep is not None else None
+
+
+def _opt(opts):
+    return ctypes.byref(opts) if opts is not None else None
+
+
+def cwc_run_state_size(model, n_replicas, sweep, t_end, sample_dt, opts=None):
+    sw = _sw(sweep)
+    n = ctypes.c_size_t()
+    _check(lib().cwc_run_state_size(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
+                                    float(sample_dt), _opt(opts), ctypes.byref(n)))
+    return n.value
+
+
+def cwc_run_init(model, n_replicas, sweep, t_end, sample_dt, state, stream, opts=None):
+    sw = _sw(sweep)
+    _check(lib().cwc_run_init(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
+                              float(sample_dt), _opt(opts), ctypes.c_void_p(state.data_ptr()), state.numel(),
+                              ctypes.c_void_p(stream)))
+
+
+def cwc_run_advance(model, n_replicas, sweep, t_end, sample_dt, seed, state, stream, quantum=0, j_stop=0, opts=None):
+    """One advance; returns how many trajectories still have samples below j_stop (synchronises the stream)."""
+    sw = _sw(sweep)
+    n_live = I64()
+    _check(lib().cwc_run_advance(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
+                                 float(sample_dt), int(seed), _opt(opts), int(quantum), int(j_stop),
+                                 ctypes.c_void_p(state.data_ptr()), state.numel(), ctypes.c_void_p(stream),
+                                 ctypes.byref(n_live)))
+    return n_live.value
+
+
+def cwc_run_stats(model, n_replicas, sweep, t_end, sample_dt, state, stats, stream, opts=None):
+    sw = _sw(sweep)
+    st = cwc_stats(stats[0].data_ptr(), stats[1].data_ptr(), stats[2].data_ptr())
+    _check(lib().cwc_run_stats(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
+                               float(sample_dt), _opt(opts), ctypes.c_void_p(state.data_ptr()), state.numel(), st,
+                               ctypes.c_void_p(stream)))
+
+
 # ---------------------------------------------------------------------------
 # convenience: allocate torch outputs and run (the calls above do the work)
 # ---------------------------------------------------------------------------
@@ -328,4 +377,63 @@ def simulate(model, n_replicas, t_end, sample_dt, seed, sweep=None, want_traj=Fa
         ci = torch.empty_like(mean)
         cwc_stats_finalize((count, sm, sq), ncell, mean, var, ci, s)
         out.update(mean=mean[:ncell].view(P_, J1, O), var=var[:ncell].view(P_, J1, O), ci90=ci[:ncell].view(P_, J1, O))
+    return out
+
+
+def simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, quantum=0, windows=None,
+                       want_traj=False, force_path=CWC_PATH_AUTO, device="cuda", checkpoint=None,
+                       kernel_events=None):
+    """Run through cwc_run_init / cwc_run_advance / cwc_run_stats.
+
+    quantum: firings per trajectory per advance (0 = unbounded); windows:
+    increasing j_stop values, one advance per window (the last is J+1), with
+    the quantum applied inside each window.  checkpoint(state, k) is called
+    after advance k and may return a replacement state tensor (e.g. one
+    restored from a host copy).  Returns the same dict as simulate() plus
+    "advances" and "live" (the pending count after each advance)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("cwc: no CUDA device (there is no CPU fallback)")
+    P_ = len(sweep["values"]) if sweep is not None else 1
+    G = P_ * int(n_replicas)
+    J1 = n_samples(t_end, sample_dt)
+    O = model.info.n_obs
+    ncell = P_ * J1 * O
+    dev = torch.device(device)
+    opts = cwc_sim_opts()
+    opts.force_path = int(force_path)
+    out = {"firings": torch.empty(G, dtype=torch.int64, device=dev),
+           "status": torch.empty(G, dtype=torch.int32, device=dev)}
+    opts.out_firings = out["firings"].data_ptr()
+    opts.out_status = out["status"].data_ptr()
+    if want_traj:
+        out["traj"] = torch.empty((G, J1, O), dtype=torch.int64, device=dev)
+        opts.out_traj = out["traj"].data_ptr()
+    if kernel_events is not None:
+        opts.ev_kernel_begin = kernel_events[0].cuda_event
+        opts.ev_kernel_end = kernel_events[1].cuda_event
+    s = torch.cuda.current_stream(dev).cuda_stream
+    state = torch.empty(cwc_run_state_size(model, n_replicas, sweep, t_end, sample_dt, opts), dtype=torch.uint8,
+                        device=dev)
+    cwc_run_init(model, n_replicas, sweep, t_end, sample_dt, state, s, opts)
+    live = []
+    wins = list(windows) if windows else [0]
+    k = 0
+    for js in wins:
+        while True:  # advance until every trajectory has passed the window (or finished)
+            n_pending = cwc_run_advance(model, n_replicas, sweep, t_end, sample_dt, seed, state, s, quantum, js, opts)
+            live.append(n_pending)
+            k += 1
+            if checkpoint is not None:
+                st2 = checkpoint(state, k)
+                if st2 is not None:
+                    state = st2
+            if n_pending == 0:
+                break
+    count = torch.empty(max(ncell, 1), dtype=torch.int64, device=dev)
+    sm = torch.empty(max(ncell, 1), dtype=torch.int64, device=dev)
+    sq = torch.empty((max(ncell, 1), 2), dtype=torch.int64, device=dev)
+    cwc_run_stats(model, n_replicas, sweep, t_end, sample_dt, state, (count, sm, sq), s, opts)
+    out.update(count=count[:ncell].view(P_, J1, O), sum=sm[:ncell].view(P_, J1, O),
+               sumsq=sq[:ncell].view(P_, J1, O, 2), n_points=P_, J1=J1, advances=k, live=live, state=state)
     return out

@@ -154,3 +154,26 @@ def test_simulate_without_gpu_fails_loudly():
     assert ei.value.status == cwc.CWC_ERR_CUDA
     with pytest.raises(RuntimeError):
         cwc.simulate(m, 16, 10.0, 1.0, 1)
+
+
+def test_run_state_size_and_errors():
+    """Resumable runs (cwc_run_*): the state buffer holds per-trajectory
+    (x, t, n, j), two live lists and the accumulators; same argument checks
+    as cwc_simulate; tracing is refused."""
+    d, sweep, cfg = w.config("C3")
+    m = cwc.cwc_model_create(d)
+    G = 16 * len(sweep["values"])
+    a = cwc.cwc_run_state_size(m, 16, sweep, 50.0, 0.5)
+    assert a >= G * (4 * m.info.n_cells + 8 + 8 + 4 + 2 * 8)
+    assert a > cwc.cwc_run_state_size(m, 16, None, 50.0, 0.5) > 0
+    for args in [(16, None, 0.0, 0.1), (16, None, 1.0, 2.0), (0, None, 1.0, 0.1)]:
+        with pytest.raises(cwc.CwcError) as ei:
+            cwc.cwc_run_state_size(m, *args)
+        assert ei.value.status == cwc.CWC_ERR_INVALID, args
+    opts = cwc.cwc_sim_opts()
+    g = np.zeros(1, dtype=np.int64)
+    opts.trace_g = g.ctypes.data
+    opts.n_trace = 1
+    with pytest.raises(cwc.CwcError) as ei:
+        cwc.cwc_run_state_size(m, 16, None, 1.0, 0.1, opts)
+    assert ei.value.status == cwc.CWC_ERR_INVALID
