@@ -55,8 +55,9 @@ constexpr int kWsGroups = CWC_WS_GROUPS;  // 32-trajectory groups (consumer + pr
 constexpr int kWsStage = 64;     // staged sample records of a consumer warp
 constexpr size_t kWsGroupBytes = (size_t)2 * kWsRing * 32 * sizeof(double) +
                                  (size_t)(kWsProducers + 2) * 32 * sizeof(unsigned) +
-                                 (size_t)kWsStage * (1 + kThreadMaxObs) * sizeof(long long);
-constexpr long long kStageLL = (long long)kWsStage * (1 + kThreadMaxObs);  // staging longs per warp
+                                 (size_t)kWsStage * (2 + kThreadMaxCells / 2) * sizeof(long long);
+// staging longs per warp: per record its first cell, its dump row, its counts (int32)
+constexpr long long kStageLL = (long long)kWsStage * (2 + kThreadMaxCells / 2);
 constexpr size_t kWsRingBytes = kWsGroups * ((kWsGroupBytes + 15) & ~(size_t)15);  // per CTA
 constexpr long long kSmemPartMaxTraj = 1ll << 16;  // trajectories per shared-memory part (16-bit limbs)
 __host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }

@@ -233,12 +233,31 @@ __device__ __forceinline__ void record_sample(const RunParams &rp, const ThreadT
     }
 }
 
+// One staged sample record, written by a lane of a full warp: the observables
+// of the staged pre-event counts, into the moments (and the optional dump).
+template <int S>
+__device__ __forceinline__ void staged_record(const RunParams &rp, const ThreadTables &tt, const StatAcc &acc,
+                                              long long cell, long long row, const int *xs) {
+    int xv[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) xv[s] = xs[s];
+    for (int o = 0; o < tt.O; ++o) {
+        long long v = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)xv[s] : 0ll;
+        stat_record(acc, cell + o, v);
+        if (rp.out_traj) rp.out_traj[row * tt.O + o] = v;
+    }
+}
+
 template <int M>
 struct ThreadBatch {
     static constexpr int B = (M <= 8) ? 4 : (M <= 16 ? 2 : 1);
 };
 
-template <int S, int M, bool TRACE>
+// RES: resumable runs (cwc_run_*: state load/save, launch bounds); the
+// one-shot instantiations carry none of it
+template <int S, int M, bool TRACE, bool RES>
 __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
     constexpr int B = ThreadBatch<M>::B;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -254,7 +273,8 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
     // staged sample records of this warp (after the statistics part)
     const long long stats_part_bytes = rp.stats_smem ? stat_bytes(rp.st, rp.cells_per_part) : 0;
     long long *st_cell = (long long *)(smem + stats_part_bytes) + (long long)(threadIdx.x >> 5) * kStageLL;
-    long long *st_v = st_cell + kWsStage;  // [kWsStage][kThreadMaxObs]
+    long long *st_row = st_cell + kWsStage;                   // [kWsStage] trajectory sample row (out_traj)
+    int *st_x = (int *)(st_row + kWsStage);                   // [kWsStage][kThreadMaxCells] pre-event counts
     const int lane = threadIdx.x & 31;
     int stage_n = 0;  // warp-uniform
 
@@ -300,16 +320,16 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         int x[S];
 #pragma unroll
         for (int s = 0; s < S; ++s)
-            x[s] = (s < tt.n_cells) ? (rp.rs_x ? rp.rs_x[g * tt.n_cells + s] : tt.init[s]) : 0;
+            x[s] = (s < tt.n_cells) ? (RES ? rp.rs_x[g * tt.n_cells + s] : tt.init[s]) : 0;
         double t = 0.0;
         long long j = 0;
         unsigned long long n = 0;
-        if (rp.rs_x) {
+        if (RES) {
             t = rp.rs_t[g];
             j = rp.rs_j[g];
             n = (unsigned long long)rp.rs_n[g];
         }
-        const long long JL = rp.j_stop - 1;  // last sample of this launch (J in one-shot runs)
+        const long long JL = RES ? rp.j_stop - 1 : J;  // last sample of this launch (J in one-shot runs)
         const unsigned long long n_start = n;
         double c[M];
 #pragma unroll
@@ -387,22 +407,18 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             // records staged in shared memory, written 32 at a time (one per lane)
             const unsigned rmask = __ballot_sync(0xffffffffu, rec);
             if (rmask) {
-                if (rec) {
+                if (rec) {  // few lanes: stage the counts only, observables are formed at the flush
                     const int slot = stage_n + __popc(rmask & ((1u << lane) - 1u));
                     st_cell[slot] = cell_base + jrec * O;
-                    for (int o = 0; o < O; ++o) {
-                        long long v = 0;
+                    st_row[slot] = g * J1 + jrec;
 #pragma unroll
-                        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)xrec[s] : 0ll;
-                        st_v[slot * kThreadMaxObs + o] = v;
-                        if (rp.out_traj) rp.out_traj[(g * J1 + jrec) * O + o] = v;
-                    }
+                    for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xrec[s];
                 }
                 stage_n += __popc(rmask);
                 if (stage_n >= 32) {
                     __syncwarp();
                     const int e = stage_n - 32 + lane;
-                    for (int o = 0; o < O; ++o) stat_record(acc, st_cell[e] + o, st_v[e * kThreadMaxObs + o]);
+                    staged_record<S>(rp, tt, acc, st_cell[e], st_row[e], st_x + e * kThreadMaxCells);
                     stage_n -= 32;
                     __syncwarp();
                 }
@@ -496,7 +512,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                 Ub[i] = Un[i];
             }
             // resumable runs: suspend after `quantum` further firings
-            if (rp.quantum > 0 && live && n - n_start >= (unsigned long long)rp.quantum) live = false;
+            if (RES && rp.quantum > 0 && live && n - n_start >= (unsigned long long)rp.quantum) live = false;
             // reconverge the warp explicitly: the vote at the loop head only
             // synchronises it, and a warp left split after the rare path would
             // run every later batch twice with half its lanes (a plain
@@ -505,13 +521,13 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         }
         __syncwarp();
         if (lane < stage_n)  // drain the staged records
-            for (int o = 0; o < O; ++o) stat_record(acc, st_cell[lane] + o, st_v[lane * kThreadMaxObs + o]);
+            staged_record<S>(rp, tt, acc, st_cell[lane], st_row[lane], st_x + lane * kThreadMaxCells);
         if (in_range) {
-            if (j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
+            if (RES && j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
-            if (rp.rs_x) {
+            if (RES) {
 #pragma unroll
                 for (int s = 0; s < S; ++s)
                     if (s < tt.n_cells) rp.rs_x[g * tt.n_cells + s] = x[s];
@@ -545,13 +561,18 @@ cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, 
         k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 64 * kWsGroups, smem, st>>>(rp, tt);
         return cudaGetLastError();
     }
-    if (trace) {
-        auto k = ssa_thread_kernel<S, M, true>;
+    if (rp.rs_x) {  // resumable runs (never traced)
+        auto k = ssa_thread_kernel<S, M, false, true>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);
+    } else if (trace) {
+        auto k = ssa_thread_kernel<S, M, true, false>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);
     } else {
-        auto k = ssa_thread_kernel<S, M, false>;
+        auto k = ssa_thread_kernel<S, M, false, false>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);

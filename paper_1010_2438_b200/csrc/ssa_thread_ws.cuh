@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
     unsigned *cons = prod + NP * 32;                   // [32] draws released
     unsigned *done = cons + 32;                        // [32] trajectory finished
     long long *st_cell = (long long *)(done + 32);     // [kWsStage] first cell of a staged record
-    long long *st_v = st_cell + kWsStage;              // [kWsStage][kThreadMaxObs] its observables
+    long long *st_row = st_cell + kWsStage;            // [kWsStage] its trajectory sample row (out_traj)
+    int *st_x = (int *)(st_row + kWsStage);            // [kWsStage][kThreadMaxCells] its pre-event counts
 
     StatAcc acc;
     long long p_base = 0;
@@ -268,22 +269,18 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
             if (prof) { c1 = clock64(); pc[1] += c1 - c0; c0 = c1; }
             const unsigned rmask = __ballot_sync(0xffffffffu, rec);
             if (rmask) {
-                if (rec) {
+                if (rec) {  // few lanes: stage the counts only, observables are formed at the flush
                     const int slot = stage_n + __popc(rmask & ((1u << lane) - 1u));
                     st_cell[slot] = cell_base + jrec * O;
-                    for (int o = 0; o < O; ++o) {
-                        long long v = 0;
+                    st_row[slot] = g * J1 + jrec;
 #pragma unroll
-                        for (int s = 0; s < S; ++s) v += (tt.obs_of[s] == o) ? (long long)xrec[s] : 0ll;
-                        st_v[slot * kThreadMaxObs + o] = v;
-                        if (rp.out_traj) rp.out_traj[(g * J1 + jrec) * O + o] = v;
-                    }
+                    for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xrec[s];
                 }
                 stage_n += __popc(rmask);
                 if (stage_n >= 32) {
                     __syncwarp();
                     const int e = stage_n - 32 + lane;
-                    for (int o = 0; o < O; ++o) stat_record(acc, st_cell[e] + o, st_v[e * kThreadMaxObs + o]);
+                    staged_record<S>(rp, tt, acc, st_cell[e], st_row[e], st_x + e * kThreadMaxCells);
                     stage_n -= 32;
                     __syncwarp();
                 }
@@ -357,7 +354,7 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
         }
         __syncwarp();
         if (lane < stage_n)  // drain the staged records
-            for (int o = 0; o < O; ++o) stat_record(acc, st_cell[lane] + o, st_v[lane * kThreadMaxObs + o]);
+            staged_record<S>(rp, tt, acc, st_cell[lane], st_row[lane], st_x + lane * kThreadMaxCells);
         if (in_range) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
