@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-                "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+                "-I", os.path.join(ROOT, "include"), "-I", CSRC] + os.environ.get("NVCC_EXTRA", "").split()
 
 
 def _sources():

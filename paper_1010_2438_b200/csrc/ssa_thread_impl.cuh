@@ -363,10 +363,15 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             unsigned bad = 0;  // bit k: firing k of the batch is not plain
             // one firing per batch may cross a single sample time that is not
             // the last: it commits, its record (pre-event state) follows the batch
+            // (at most one: it is the batch's only change of j, so the
+            // per-firing bookkeeping is a few selects; the batch-start sample
+            // times are kept for a rollback, and t_next3 = (j + 2) dt becomes
+            // the next-but-one sample time after the crossing)
             bool rec = false;
             int krec = B;
-            long long jrec = 0;
-            int xrec[S];
+            const bool jok = j < JL;
+            const double t_next0 = t_next, t_next20 = t_next2;
+            const double t_next3 = __dmul_rn(__ll2double_rn(j + 2), rp.dt);
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
@@ -377,17 +382,11 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                 tsnap[k] = t;
                 bool cross1;
                 const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
-                const bool take = cross1 && !rec && (j < JL);
-                if (take) {
-                    rec = true;
-                    krec = k;
-                    jrec = j;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) xrec[s] = xsnap[k][s];
-                    j += 1;
-                    t_next = t_next2;
-                    t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
-                }
+                const bool take = cross1 && !rec && jok;
+                rec = rec || take;
+                krec = take ? k : krec;
+                t_next = take ? t_next2 : t_next;
+                t_next2 = take ? t_next3 : t_next2;
                 // TRACE builds take every firing through the exact path below
                 // (it writes the trace)
                 bad |= (!TRACE && (plain || take)) ? 0u : (1u << k);
@@ -396,10 +395,11 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
             if (rec && krec >= used) {  // the crossing firing was rolled back
                 rec = false;
-                j = jrec;
-                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
-                t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+                t_next = t_next0;
+                t_next2 = t_next20;
             }
+            const long long jrec = j;  // the sample a committed crossing recorded
+            if (rec) j += 1;
             if (live) {
                 n += (unsigned long long)used;
                 firings += used;
@@ -412,7 +412,11 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                     st_cell[slot] = cell_base + jrec * O;
                     st_row[slot] = g * J1 + jrec;
 #pragma unroll
-                    for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xrec[s];
+                    for (int k = 0; k < B; ++k)  // pre-event counts of firing krec
+                        if (k == krec) {
+#pragma unroll
+                            for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xsnap[k][s];
+                        }
                 }
                 stage_n += __popc(rmask);
                 if (stage_n >= 32) {

@@ -25,6 +25,10 @@
 #pragma once
 #include "ssa_thread_impl.cuh"
 
+#ifndef CWC_WS_PROF
+#define CWC_WS_PROF 0  // consumer cycle accounting (tools/ws_prof.py; debug builds)
+#endif
+
 #ifndef CWC_WS_MINB
 #define CWC_WS_MINB 6  // CTAs per SM the register budget must allow for small models (S*M <= 12:
                        // <= 170 registers; 1 and 8 measured slower); larger models get the full budget
@@ -185,7 +189,9 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
         // [0] waiting for draws, [1] fast batch, [2] records, [3] exact path,
         // [4] batches, [5] total
         unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
-        const bool prof = rp.prof != nullptr;
+        // (compiled in only with -DCWC_WS_PROF=1: the checks cost ~2 % of the
+        // consumer's instructions)
+        const bool prof = CWC_WS_PROF && rp.prof != nullptr;
         long long c0 = prof ? clock64() : 0, c1 = 0;
         const long long c_start = c0;
         while (__any_sync(0xffffffffu, live)) {
@@ -226,10 +232,15 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
             int xsnap[B][S];
             double tsnap[B];
             unsigned bad = 0;
+            // (at most one: it is the batch's only change of j, so the
+            // per-firing bookkeeping is a few selects; the batch-start sample
+            // times are kept for a rollback, and t_next3 = (j + 2) dt becomes
+            // the next-but-one sample time after the crossing)
             bool rec = false;
             int krec = B;
-            long long jrec = 0;
-            int xrec[S];
+            const bool jok = j < J;
+            const double t_next0 = t_next, t_next20 = t_next2;
+            const double t_next3 = __dmul_rn(__ll2double_rn(j + 2), rp.dt);
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
@@ -237,27 +248,22 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
                 tsnap[k] = t;
                 bool cross1;
                 const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
-                const bool take = cross1 && !rec && (j < J);
-                if (take) {
-                    rec = true;
-                    krec = k;
-                    jrec = j;
-#pragma unroll
-                    for (int s = 0; s < S; ++s) xrec[s] = xsnap[k][s];
-                    j += 1;
-                    t_next = t_next2;
-                    t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
-                }
+                const bool take = cross1 && !rec && jok;
+                rec = rec || take;
+                krec = take ? k : krec;
+                t_next = take ? t_next2 : t_next;
+                t_next2 = take ? t_next3 : t_next2;
                 bad |= (plain || take) ? 0u : (1u << k);
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;
             if (rec && krec >= used) {  // the crossing firing was rolled back
                 rec = false;
-                j = jrec;
-                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
-                t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
+                t_next = t_next0;
+                t_next2 = t_next20;
             }
+            const long long jrec = j;  // the sample a committed crossing recorded
+            if (rec) j += 1;
             if (live) {
                 n += (unsigned long long)used;
                 firings += used;
@@ -274,7 +280,11 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
                     st_cell[slot] = cell_base + jrec * O;
                     st_row[slot] = g * J1 + jrec;
 #pragma unroll
-                    for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xrec[s];
+                    for (int k = 0; k < B; ++k)  // pre-event counts of firing krec
+                        if (k == krec) {
+#pragma unroll
+                            for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xsnap[k][s];
+                        }
                 }
                 stage_n += __popc(rmask);
                 if (stage_n >= 32) {

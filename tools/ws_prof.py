@@ -1,5 +1,7 @@
 """Cycle accounting of the warp-specialised consumer (debug hook CWC_PROF_PTR).
 
+Needs a library built with the accounting compiled in:
+    NVCC_EXTRA=-DCWC_WS_PROF=1 python -c "from paper_1010_2438_b200 import _build; _build.build(force=True)"
     python tools/ws_prof.py --config C2 [--t-end 2]
 """
 import argparse
