@@ -286,6 +286,9 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
             }
             for (int wd = 0; wd < kOpWords; ++wd) tt.op_pack[k][wd] = op[wd];
         }
+        const int s_pad = thread_pad_cells(ncell), m_pad = thread_pad_reactions(std::max(M, 2));
+        if (s_pad > 0 && m_pad > 0 && 8 * s_pad + 16 * m_pad <= 64)
+            for (int k = 0; k < M; ++k) tt.comb_pack[k] = tt.nu_pack[k] | (tt.op_pack[k][0] << (8 * s_pad));
         for (int c = 0; c < kThreadMaxCells; ++c) {
             tt.obs_of[c] = c < ncell ? m->obs_of_cell[c] : -1;
             tt.init[c] = c < ncell ? m->init[c] : 0;

@@ -147,6 +147,10 @@ struct ThreadTables {
     // for an absent reactant) -- the kernel then keeps the operands
     // themselves as state instead of gathering them from x
     uint64_t op_pack[kThreadMaxReactions][kOpWords];
+    // nu_pack and op_pack word 0 in ONE word when 8 S_pad + 16 M_pad <= 64
+    // (C1, C2): net change bytes 0 .. S_pad-1, operand deltas from byte
+    // S_pad on -- the selection then moves one word per compare
+    uint64_t comb_pack[kThreadMaxReactions];
     int32_t obs_of[kThreadMaxCells];
     int32_t init[kThreadMaxCells];
 };

@@ -143,7 +143,8 @@ template <int S, int M>
 struct FastChain {
     static constexpr bool OPND = (M <= 4 * kOpWords);
     static constexpr int NW = OPND ? (M + 3) / 4 : 1;  // operand delta words in use
-    int A[M], Bo[M];
+    static constexpr bool COMB = OPND && 8 * S + 16 * M <= 64;  // ThreadTables.comb_pack
+    int A[M], Bo[M];  // operands x[ia_m] and x[ib_m] - sub_m
     // k_m * 2^-shr_m (exact scaling): then a_m = k_m' * RN(x_a (x_b - sub)),
     // which equals k_m * RN(x_a (x_b - sub) / 2^shr) bit for bit (halving
     // commutes with rounding), with no 64-bit shift in the chain
@@ -159,7 +160,7 @@ struct FastChain {
 #pragma unroll
             for (int m = 0; m < M; ++m) {
                 A[m] = pick(x, tt.ia[m]);
-                Bo[m] = pick(x, tt.ib[m]);
+                Bo[m] = pick(x, tt.ib[m]) - tt.sub[m];
             }
         }
     }
@@ -179,7 +180,7 @@ struct FastChain {
         if constexpr (OPND) {
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const double a = __dmul_rn(ch[m], __ll2double_rn((long long)A[m] * (long long)(Bo[m] - tt.sub[m])));
+                const double a = __dmul_rn(ch[m], __ll2double_rn((long long)A[m] * (long long)Bo[m]));
                 cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
             }
         } else {
@@ -188,16 +189,25 @@ struct FastChain {
         const double a0 = cum[M - 1];
         const double tn = __dadd_rn(t, div_fast(E, a0));
         const double target = __dmul_rn(U, a0);
-        unsigned long long nu = tt.nu_pack[0], op[NW];
+        unsigned long long nu, op[NW];
+        if constexpr (COMB) {
+            unsigned long long cw = tt.comb_pack[0];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) op[w] = tt.op_pack[0][w];
+            for (int m = 0; m + 1 < M; ++m) cw = (cum[m] <= target) ? tt.comb_pack[m + 1] : cw;
+            nu = cw;                // bytes 0 .. S-1 (apply_nu reads no more)
+            op[0] = cw >> (8 * S);  // operand deltas
+        } else {
+            nu = tt.nu_pack[0];
 #pragma unroll
-        for (int m = 0; m + 1 < M; ++m) {
-            const bool past = cum[m] <= target;
-            nu = past ? tt.nu_pack[m + 1] : nu;
-            if constexpr (OPND) {
+            for (int w = 0; w < NW; ++w) op[w] = tt.op_pack[0][w];
 #pragma unroll
-                for (int w = 0; w < NW; ++w) op[w] = past ? tt.op_pack[m + 1][w] : op[w];
+            for (int m = 0; m + 1 < M; ++m) {
+                const bool past = cum[m] <= target;
+                nu = past ? tt.nu_pack[m + 1] : nu;
+                if constexpr (OPND) {
+#pragma unroll
+                    for (int w = 0; w < NW; ++w) op[w] = past ? tt.op_pack[m + 1][w] : op[w];
+                }
             }
         }
         int xn[S];
