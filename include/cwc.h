@@ -247,6 +247,13 @@ cwc_status cwc_philox_blocks(uint64_t seed, const int64_t *g, const int64_t *n, 
 cwc_status cwc_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
                      void *cuda_stream);
 
+/* Uniforms u1[i], u2[i] (reading 3) and E[i] = -log u1[i] of the raw
+ * Philox output blocks words[i][0..3] (device uint32 [count][4]; device double
+ * outputs), formed exactly as the SSA kernels form them.  Test hook for the
+ * conversion edges (all-zero and all-one words, the top bit). */
+cwc_status cwc_block_draws(const uint32_t *words, int64_t count, double *u1, double *u2, double *E,
+                           void *cuda_stream);
+
 /* q[i] = e[i] / a[i] computed the way the SSA kernels compute tau = E / a0
  * (P:206-207): the branch-free fast division where its range guard holds,
  * IEEE div.rn otherwise.  Must equal the IEEE quotient bit for bit.  Device

@@ -1076,6 +1076,13 @@ cwc_status cwc_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t 
     return CWC_OK;
 }
 
+cwc_status cwc_block_draws(const uint32_t *words, int64_t count, double *u1, double *u2, double *E, void *cuda_stream) {
+    if (count < 0 || (count > 0 && (!words || !u1 || !u2 || !E))) return fail(CWC_ERR_INVALID, "bad arguments");
+    cudaError_t e = launch_block_draws(words, count, u1, u2, E, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cwc_block_draws");
+    return CWC_OK;
+}
+
 cwc_status cwc_tau_div(const double *num, const double *den, int64_t count, double *q, void *cuda_stream) {
     if (count < 0 || (count > 0 && (!num || !den || !q))) return fail(CWC_ERR_INVALID, "bad arguments");
     cudaError_t e = launch_tau_div(num, den, count, q, (cudaStream_t)cuda_stream);

@@ -47,7 +47,10 @@ __host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, lo
 // warp-specialised thread path (ssa_thread_ws.cuh): draws in flight per
 // trajectory and the ring + hand-off counters' shared-memory bytes per CTA
 constexpr int kWsRing = 32;
-constexpr int kWsProducers = 1;  // producer warps per group (2 measured slower on C2)
+#ifndef CWC_WS_PRODUCERS
+#define CWC_WS_PRODUCERS 1
+#endif
+constexpr int kWsProducers = CWC_WS_PRODUCERS;  // producer warps per group
 #ifndef CWC_WS_GROUPS
 #define CWC_WS_GROUPS 1
 #endif
@@ -198,6 +201,7 @@ cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t 
 cudaError_t launch_draws(uint64_t seed, const int64_t *g, const int64_t *n, int64_t count, double *E, double *u2,
                          cudaStream_t stream);
 cudaError_t launch_tau_div(const double *e, const double *a, int64_t count, double *q, cudaStream_t stream);
+cudaError_t launch_block_draws(const uint32_t *w, int64_t count, double *u1, double *u2, double *E, cudaStream_t stream);
 
 // resume.cu: resumable runs (state initialisation, live-list compaction)
 cudaError_t launch_state_init(long long G, int n_cells, const int32_t *init, int32_t *x, double *t, int64_t *n,

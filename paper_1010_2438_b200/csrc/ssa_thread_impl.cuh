@@ -572,7 +572,7 @@ cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, 
         auto k = ssa_thread_ws_kernel<S, M>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 64 * kWsGroups, smem, st>>>(rp, tt);
+        k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 32 * (1 + kWsProducers) * kWsGroups, smem, st>>>(rp, tt);
         return cudaGetLastError();
     }
     if (rp.rs_x) {  // resumable runs (never traced)

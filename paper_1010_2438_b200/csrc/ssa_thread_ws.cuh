@@ -58,7 +58,7 @@ __device__ __forceinline__ void st_relaxed(unsigned *p, unsigned v) {
 }
 
 template <int S, int M>
-__global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / kWsGroups > 1) ? CWC_WS_MINB / kWsGroups : 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
+__global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <= 12 && CWC_WS_MINB / kWsGroups / kWsProducers > 1) ? CWC_WS_MINB / kWsGroups / kWsProducers : 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
     // consumer batch B; one producer warp per group computes rounds of PW
     // draws (round r = draws [r PW, r PW + PW) of each of its trajectories)
     constexpr int B = ThreadBatch<M>::B;
@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
     constexpr int K = kWsRing;
     constexpr int GPC = kWsGroups;  // 32-trajectory groups per CTA
     static_assert(K >= B + NP * PW && (K & (K - 1)) == 0 && B <= PW, "ring too small");
+    static_assert(NP == 1 || GPC == 1, "several producers: one group per CTA");
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -87,9 +88,11 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
     // (warp id mod 4) then holds producer k and consumer k, and the consumer,
     // with the higher warp id, wins the issue arbitration (highest warp id
     // first) whenever both are ready: the producer fills the consumer's gaps
-    const int grp = (GPC == 4) ? (warp & 3) : (warp >> 1);
-    const bool consumer = (GPC == 4) ? (warp >= 4)
-                                     : ((((unsigned)(warp & 1) ^ (unsigned)grp) & 1u) == pattern);
+    // NP > 1 (one group per CTA): warp 0 consumes, warps 1 .. NP produce
+    const int grp = (NP > 1) ? 0 : (GPC == 4) ? (warp & 3) : (warp >> 1);
+    const bool consumer = (NP > 1) ? (warp == 0)
+                          : (GPC == 4) ? (warp >= 4)
+                                       : ((((unsigned)(warp & 1) ^ (unsigned)grp) & 1u) == pattern);
 
     // dispatch order: CTA slot blockIdx.x runs trajectory block cta (RunParams.cta_order)
     const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(64 * kWsGroups, (S * M <= 12 && CWC_WS_MINB / 
 
     if (!consumer) {
         // ---------------- producer ----------------
-        const int q = 0;
+        const int q = (NP > 1) ? warp - 1 : 0;  // this producer's rounds: q, q + NP, q + 2 NP, ...
         unsigned rounds = 0;  // rounds done by this producer (its counter; differences wrap)
         for (;;) {
             const bool act = ld_acquire(done + lane) == 0u;

@@ -169,6 +169,24 @@ __global__ void draws_kernel(uint64_t seed, const int64_t *g, const int64_t *n, 
     }
 }
 
+__global__ void block_draws_kernel(const uint32_t *w, long long count, double *u1, double *u2, double *E) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+        double a, b;
+        block_uniforms(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3], a, b);
+        u1[i] = a;
+        u2[i] = b;
+        E[i] = neg_log_unit(a);
+    }
+}
+
+cudaError_t launch_block_draws(const uint32_t *w, int64_t count, double *u1, double *u2, double *E, cudaStream_t stream) {
+    if (count == 0) return cudaSuccess;
+    long long blocks = (count + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    block_draws_kernel<<<(unsigned)blocks, 256, 0, stream>>>(w, count, u1, u2, E);
+    return cudaGetLastError();
+}
+
 __global__ void tau_div_kernel(const double *e, const double *a, long long count, double *q) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
         const double x = e[i], y = a[i];

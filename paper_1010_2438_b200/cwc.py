@@ -24,7 +24,7 @@ CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
 
 EXPORTED = ["cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
             "cwc_simulate_workspace_size", "cwc_simulate", "cwc_simulate_host", "cwc_simulate_host_workspace_size",
-            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_tau_div", "cwc_run_state_size",
+            "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_block_draws", "cwc_tau_div", "cwc_run_state_size",
             "cwc_run_init", "cwc_run_advance", "cwc_run_stats", "cwc_last_error"]
 
 P = ctypes.c_void_p
@@ -91,6 +91,7 @@ def lib():
         L.cwc_philox_blocks.argtypes = [ctypes.c_uint64, P, P, I64, P, P]
         L.cwc_draws.argtypes = [ctypes.c_uint64, P, P, I64, P, P, P]
         L.cwc_tau_div.argtypes = [P, P, I64, P, P]
+        L.cwc_block_draws.argtypes = [P, I64, P, P, P, P]
         D = ctypes.c_double
         L.cwc_run_state_size.argtypes = [P, I64, P, D, D, P, ctypes.POINTER(ctypes.c_size_t)]
         L.cwc_run_init.argtypes = [P, I64, P, D, D, P, P, ctypes.c_size_t, P]
@@ -261,6 +262,11 @@ def cwc_philox_blocks(seed, g, n, out, stream):
 
 def cwc_draws(seed, g, n, E, u2, stream):
     _check(lib().cwc_draws(int(seed), _ptr(g), _ptr(n), int(g.numel()), _ptr(E), _ptr(u2), ctypes.c_void_p(stream)))
+
+
+def cwc_block_draws(words, u1, u2, E, stream):
+    """words: uint32-valued torch tensor [count, 4] (int32 storage) on the device."""
+    _check(lib().cwc_block_draws(_ptr(words), int(words.shape[0]), _ptr(u1), _ptr(u2), _ptr(E), ctypes.c_void_p(stream)))
 
 
 def cwc_tau_div(e, a, q, stream):

@@ -106,3 +106,28 @@ def test_draws_match_oracle_and_are_accurate():
         ulp = mpmath.mpf(2) ** (mpmath.floor(mpmath.log(ex, 2)) - 52)
         worst = max(worst, float(abs(mpmath.mpf(float(E[i])) - ex) / ulp))
     assert worst < 1.0, worst
+
+
+def test_uniform_conversion_edges_match_oracle():
+    """u1, u2 of raw blocks at the conversion edges (all-zero / all-one
+    words, the top bit, the 11 dropped bits) equal the oracle's exactly, and
+    E = -log u1 stays within one ulp of the oracle's log (u1 = 2^-53 and 1)."""
+    edge = [0x00000000, 0xFFFFFFFF, 0x80000000, 0x7FFFFFFF, 0x000007FF, 0x00000800, 0xFFFFF800, 0x00100000]
+    rng = np.random.default_rng(5)
+    words = [[a, b, c, d] for a in edge for b in edge for c, d in [(a, b), (b, a)]]
+    words += rng.integers(0, 2**32, size=(20000, 4), dtype=np.uint64).tolist()
+    w = np.asarray(words, dtype=np.uint64).astype(np.uint32)
+    wt = torch.as_tensor(w.view(np.int32), device="cuda")
+    u1 = torch.empty(len(w), dtype=torch.float64, device="cuda")
+    u2 = torch.empty_like(u1)
+    E = torch.empty_like(u1)
+    cwc.cwc_block_draws(wt, u1, u2, E, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    u1, u2, E = u1.cpu().numpy(), u2.cpu().numpy(), E.cpu().numpy()
+    want = np.array([oracle.uniforms(x) for x in w])
+    assert np.array_equal(u1.view(np.int64), want[:, 0].view(np.int64))
+    assert np.array_equal(u2.view(np.int64), want[:, 1].view(np.int64))
+    assert u1.min() == 2.0**-53 and u1.max() == 1.0 and u2.min() == 0.0 and u2.max() == 1.0 - 2.0**-53
+    ref = -np.log(want[:, 0])
+    assert _ulps(E, ref).max() <= 1
+    assert E[u1 == 1.0].max() == 0.0
