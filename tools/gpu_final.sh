@@ -18,3 +18,9 @@ for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do
   ncu --set full --clock-control none --import-source on -k regex:ssa_ -c 1 -o $OUT/full_$c \
       python tools/run_case.py --config $c > $OUT/ncu_$c.log 2>&1; echo full_$c=$?
 done
+# summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB return limit):
+# counters per config, per-source-line tables, and only the default config's report
+python tools/ncu_summary.py $OUT/ncu_full_summary.json $(for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && echo $c=$OUT/full_$c.ncu-rep; done) > $OUT/ncu_summary.log 2>&1; echo summary=$?
+for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && python tools/ncu_lines.py $OUT/full_$c.ncu-rep 60 > $OUT/lines_$c.txt 2>&1; done
+mkdir -p $OUT/../reps_${TAG:-final}
+for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ "$c" != "C2" ] && rm -f $OUT/full_$c.ncu-rep; done
