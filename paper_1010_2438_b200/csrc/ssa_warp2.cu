@@ -87,20 +87,25 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     }
     int *xs = (int *)(smem + stats_smem_bytes + (long long)(wib * 2 + seg) * per_seg_bytes);
     double *as = (double *)((unsigned char *)xs + x_bytes);
-    double2 *dr = (double2 *)(as + 16 * Bp);  // [32] the segment's draws (E, u2) of firings n_base ..
+    double2 *dr = (double2 *)(as + 16 * Bp);  // [32] the segment's draws (E, u2) of firings n - kd ..
     __shared__ unsigned int cta_traj;  // trajectories taken by this CTA (shared-memory part capacity)
+    __shared__ unsigned long long q_stop[32];  // per segment: resumable runs' firing bound
     if (threadIdx.x == 0) cta_traj = 0;
     __syncthreads();
 
     // per-segment trajectory state (uniform over the segment's 16 lanes)
     bool active = false, exhausted = false;
-    long long g = 0, cell_base = 0;
+    long long g = 0;
     const double *rates = rp.rates;
     uint64_t gk = 0;
     double t = 0.0, t_next = 0.0, a0 = 0.0, incl = 0.0, excl = 0.0, part = 0.0;
-    long long j = 0, firings = 0;
-    unsigned long long n = 0, n_base = 0, n_start = 0;
-    const long long JL = rp.j_stop - 1;  // last sample of this launch (J in one-shot runs)
+    // (kept lean: the kernel runs at 64 registers, and every live 64-bit
+    // value pushes index arithmetic into rematerialisation.  n counts the
+    // applied firings = the next draw's counter; kd = draws used from the
+    // 32-draw window; samples j < rp.j_stop are recorded in this launch, J+1
+    // in one-shot runs; a resumable run's firing bound sits in shared memory)
+    int j = 0, kd = 0;
+    unsigned long long n = 0;
 
     // divergence tracer (TRACE builds): per-firing records (n, a0, tau, t', mu)
     // of the trajectories listed in rp.trace_g, written by the segment's lane 0
@@ -116,18 +121,19 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         }
     };
 
-    auto record = [&](long long jj) {
+    auto record = [&](int jj) {  // rare: the statistics cell is recomputed from g
+        const long long cb = (g / rp.R) * J1 * O + (long long)jj * O;
         for (int o = sl; o < O; o += 16) {
             long long v = 0;
             for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xs[__ldg(wt.obs_cells + q)];
-            stat_record(acc, cell_base + jj * O + o, v);
+            stat_record(acc, cb + o, v);
             if (rp.out_traj) rp.out_traj[(g * J1 + jj) * O + o] = v;
         }
     };
     auto finish = [&](int status) {  // the segment's trajectory ended or is suspended
         if (j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;
         if (sl == 0) {
-            if (rp.out_firings) rp.out_firings[g] = firings;
+            if (rp.out_firings) rp.out_firings[g] = (int64_t)n;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
         }
@@ -159,7 +165,6 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                 g = launch_traj(rp, (long long)gg);
                 const long long p = g / rp.R;
                 rates = rp.rates + p * M;
-                cell_base = p * J1 * O;
                 gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);
                 if (TRACE) {
                     tslot = -1;
@@ -196,40 +201,39 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                     j = rp.rs_j[g];
                     n = (unsigned long long)rp.rs_n[g];
                 }
-                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
-                firings = (long long)n;
-                n_base = n;
-                n_start = n;
+                t_next = __dmul_rn(__int2double_rn(j), rp.dt);
+                kd = 0;
+                if (sl == 0) q_stop[wib * 2 + seg] = rp.quantum > 0 ? n + (unsigned long long)rp.quantum : ~0ull;
                 double e0, u0, e1, u1;
-                block_to_draws(philox_block(rp.seed, gk, n_base + sl), e0, u0);
-                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), e1, u1);
+                block_to_draws(philox_block(rp.seed, gk, n + sl), e0, u0);
+                block_to_draws(philox_block(rp.seed, gk, n + 16 + sl), e1, u1);
                 dr[sl] = make_double2(e0, u0);
                 dr[16 + sl] = make_double2(e1, u1);
                 active = true;
-                if (j > JL) finish(CWC_TRAJ_DONE);  // resumed at its launch's sample bound
+                if (j >= rp.j_stop) finish(CWC_TRAJ_DONE);  // resumed at its launch's sample bound
             }
             __syncwarp();
         }
         if (!__any_sync(kAll, active)) break;
 
         // ---- one firing of each active segment ----
-        const bool refill = active && (n - n_base == 32);
+        const bool refill = active && kd == 32;
         if (__any_sync(kAll, refill)) {
             // resumable runs: suspend after `quantum` further firings (at a
             // 32-draw window boundary)
-            if (refill && rp.quantum > 0 && n - n_start >= (unsigned long long)rp.quantum) {
+            if (refill && n >= q_stop[wib * 2 + seg]) {
                 finish(CWC_TRAJ_DONE);
             } else if (refill) {
-                n_base = n;
+                kd = 0;
                 double e0, u0, e1, u1;
-                block_to_draws(philox_block(rp.seed, gk, n_base + sl), e0, u0);
-                block_to_draws(philox_block(rp.seed, gk, n_base + 16 + sl), e1, u1);
+                block_to_draws(philox_block(rp.seed, gk, n + sl), e0, u0);
+                block_to_draws(philox_block(rp.seed, gk, n + 16 + sl), e1, u1);
                 dr[sl] = make_double2(e0, u0);
                 dr[16 + sl] = make_double2(e1, u1);
             }
             __syncwarp();
         }
-        const int i = (int)(n - n_base);  // segment-uniform
+        const int i = kd;  // segment-uniform
         const double2 d2 = dr[i & 31];      // broadcast read (all lanes of the segment, one address)
         const double E = d2.x, u2 = d2.y;
         const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
@@ -239,20 +243,20 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         if (__any_sync(kAll, cross)) {
             if (cross) {  // divergent: no warp-wide intrinsics inside
                 if (a0 == 0.0) {  // stall
-                    for (; j <= JL; ++j) record(j);
+                    for (; j < rp.j_stop; ++j) record(j);
                     finish(CWC_TRAJ_STALLED);
                     fire = false;
                 } else {
-                    while (j <= JL && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                    while (j < rp.j_stop && __dmul_rn(__int2double_rn(j), rp.dt) <= tn) {
                         record(j);
                         ++j;
                     }
-                    if (j > JL) {  // horizon (or the launch's last sample) reached: drawn, not applied
+                    if (j >= rp.j_stop) {  // horizon (or the launch's last sample) reached: drawn, not applied
                         trace_rec(n, a0, tau, tn, -1);
                         finish(CWC_TRAJ_DONE);
                         fire = false;
                     } else {
-                        t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                        t_next = __dmul_rn(__int2double_rn(j), rp.dt);
                     }
                 }
             }
@@ -285,7 +289,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         const bool ovf = ((__ballot_sync(kAll, nv > 0x7fffffffll) >> sb) & 0xffffu) != 0u;
         if (__any_sync(kAll, ovf)) {
             if (ovf) {  // a count would leave int32: freeze + fill
-                for (; j <= JL; ++j) record(j);
+                for (; j < rp.j_stop; ++j) record(j);
                 finish(CWC_TRAJ_OVERFLOW);
                 fire = false;
             }
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         if (sl == 0) excl = 0.0;
         if (fire) {
             t = tn;
-            ++firings;
+            ++kd;
             ++n;
         }
         asm volatile("bar.warp.sync -1;" ::: "memory");  // keep the warp converged
