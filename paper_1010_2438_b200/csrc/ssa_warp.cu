@@ -19,7 +19,7 @@
 //
 // One firing (Fig. fig:simd P:608-621):
 //   tau = E_n / a0 (E_n = -log u1 of Philox block n, drawn 32 at a time: lane
-//   i computes block n_base + i, then broadcast by shuffle), sample crossing
+//   i computes block n - kd + i, then broadcast by shuffle), sample crossing
 //   into the moment accumulators, target = u2 a0,
 //   L = ffs(ballot(prefix_l > target)) picks the chunk; the lanes then read
 //   chunk L (lane k <- a[L*Bp + k]), shuffle-scan it from L's exclusive
@@ -129,7 +129,6 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         const long long g = RES ? launch_traj(rp, (long long)gg) : (long long)gg;
         const long long p = g / rp.R;
         const double *rates = rp.rates + p * M;
-        const long long cell_base = p * J1 * O;
         const uint64_t gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);  // RNG stream id
 
         int tslot = -1;
@@ -154,8 +153,10 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         for (int c = lane; c < wt.n_cells; c += 32)
             xs[c] = RES ? rp.rs_x[g * wt.n_cells + c] : __ldg(wt.init + c);
         if (lane == 0) xs[wt.n_cells] = 1;
+        // (lean state -- see ssa_warp2.cu: n = applied firings = next draw
+        // counter, kd = draws used from the 32-draw window, 32-bit j)
         double t = 0.0;
-        long long j = 0;
+        int j = 0;
         unsigned long long n = 0;
         if (RES) {
             t = rp.rs_t[g];
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         }
         // resumable bounds: samples j < jend in this launch (J+1 in one-shot
         // runs); the quantum's firing bound sits in shared memory
-        const long long jend = RES ? (long long)rp.j_stop : J1;
+        const int jend = RES ? (int)rp.j_stop : (int)J1;
         if (RES && lane == 0) q_stop[wib] = rp.quantum > 0 ? n + (unsigned long long)rp.quantum : ~0ull;
         __syncwarp();
 
@@ -181,33 +182,33 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         if (lane == 0) excl = 0.0;
         __syncwarp();
 
-        auto record = [&](long long j) {
+        auto record = [&](int jj) {  // rare: the statistics cell is recomputed from g
+            const long long cb = (g / rp.R) * J1 * O + (long long)jj * O;
             for (int o = lane; o < O; o += 32) {
                 long long v = 0;
                 for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xs[__ldg(wt.obs_cells + q)];
-                stat_record(acc, cell_base + j * O + o, v);
-                if (rp.out_traj) rp.out_traj[(g * J1 + j) * O + o] = v;
+                stat_record(acc, cb + o, v);
+                if (rp.out_traj) rp.out_traj[(g * J1 + jj) * O + o] = v;
             }
         };
 
-        double t_next = RES ? __dmul_rn(__ll2double_rn(j), rp.dt) : 0.0;
-        unsigned long long n_base = n;
-        long long firings = (long long)n;
+        double t_next = RES ? __dmul_rn(__int2double_rn(j), rp.dt) : 0.0;
+        int kd = 0;
         int status = CWC_TRAJ_DONE;
         double El, u2l;
-        block_to_draws(philox_block(rp.seed, gk, n_base + lane), El, u2l);
+        block_to_draws(philox_block(rp.seed, gk, n + lane), El, u2l);
 
         // (a trajectory resumed at its launch's sample bound -- j_stop
         // windows -- has nothing to do)
         if (!RES || j < jend) for (;;) {
-            if (n - n_base == 32) {
+            if (kd == 32) {
                 // resumable runs: suspend after `quantum` further firings (at a
                 // 32-draw window boundary)
                 if (RES && n >= q_stop[wib]) break;
-                n_base = n;
-                block_to_draws(philox_block(rp.seed, gk, n_base + lane), El, u2l);
+                kd = 0;
+                block_to_draws(philox_block(rp.seed, gk, n + lane), El, u2l);
             }
-            const int i = (int)(n - n_base);
+            const int i = kd;
             const double E = shfl_d(El, i);
             const double u2 = shfl_d(u2l, i);
             // warp-uniform operands: the fast/IEEE choice never diverges
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
                     status = CWC_TRAJ_STALLED;
                     break;
                 }
-                while (j < jend && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
+                while (j < jend && __dmul_rn(__int2double_rn(j), rp.dt) <= tn) {
                     record(j);
                     ++j;
                 }
@@ -228,7 +229,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
                     status = CWC_TRAJ_DONE;
                     break;
                 }
-                t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
+                t_next = __dmul_rn(__int2double_rn(j), rp.dt);
             }
             const double target = __dmul_rn(u2, a0);
             const int L = __ffs(__ballot_sync(kFull, incl > target)) - 1;  // lane 31's prefix is a0 > target
@@ -312,13 +313,13 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             if (lane == 0) excl = 0.0;
 
             t = tn;
-            ++firings;
+            ++kd;
             ++n;
             asm volatile("bar.warp.sync -1;" ::: "memory");  // keep the warp converged
         }
         if (RES && j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
         if (lane == 0) {
-            if (rp.out_firings) rp.out_firings[g] = firings;
+            if (rp.out_firings) rp.out_firings[g] = (int64_t)n;
             if (rp.out_status) rp.out_status[g] = status;
             if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
         }
