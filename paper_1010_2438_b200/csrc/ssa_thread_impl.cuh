@@ -243,6 +243,45 @@ __device__ __forceinline__ void record_sample(const RunParams &rp, const ThreadT
     }
 }
 
+// Stall fill, warp-cooperative: every lane in fm has stalled
+// at sample j with frozen counts x; its remaining samples j .. JL all take
+// the same observables.  The whole (converged) warp writes them, one sample
+// per lane per pass, instead of the stalled lane alone (C3: trajectories
+// whose substrate is used up stall early and fill up to 100 samples each).
+template <int S>
+__device__ __forceinline__ void stall_fill(const RunParams &rp, const ThreadTables &tt, const StatAcc &acc,
+                                           unsigned fm, const int (&x)[S], long long cell_base, long long g,
+                                           long long j, long long JL, int lane) {
+    const int O = tt.O;
+    const long long J1 = (long long)rp.J + 1;
+    long long v[kThreadMaxObs];
+#pragma unroll
+    for (int o = 0; o < kThreadMaxObs; ++o) {
+        v[o] = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s) v[o] += (tt.obs_of[s] == o) ? (long long)x[s] : 0ll;
+    }
+    while (fm) {
+        const int src = __ffs(fm) - 1;
+        fm &= fm - 1u;
+        const long long cb = __shfl_sync(0xffffffffu, cell_base, src);
+        const long long gs = __shfl_sync(0xffffffffu, g, src);
+        const long long j0 = __shfl_sync(0xffffffffu, j, src);
+        long long vs[kThreadMaxObs];
+#pragma unroll
+        for (int o = 0; o < kThreadMaxObs; ++o) vs[o] = __shfl_sync(0xffffffffu, v[o], src);
+        for (long long jj = j0 + lane; jj <= JL; jj += 32) {
+#pragma unroll
+            for (int o = 0; o < kThreadMaxObs; ++o) {
+                if (o < O) {
+                    stat_record(acc, cb + jj * O + o, vs[o]);
+                    if (rp.out_traj) rp.out_traj[(gs * J1 + jj) * O + o] = vs[o];
+                }
+            }
+        }
+    }
+}
+
 // One staged sample record, written by a lane of a full warp: the observables
 // of the staged pre-event counts, into the moments (and the optional dump).
 template <int S>
@@ -441,6 +480,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             // ---- rare: roll back to the first non-plain firing, run ONE exact
             // iteration (the oracle's loop body) and shift the draws ----
             if (__any_sync(0xffffffffu, bad != 0u)) {
+                bool fill = false;  // stalled here: samples j .. JL filled below, warp-wide
                 double E = Eb[0], u2 = Ub[0];  // draw of firing n (= batch slot `used`)
                 if (bad != 0u) {
 #pragma unroll
@@ -459,7 +499,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                     cumulative(tt, gt, x, c, cum);
                     const double a0 = cum[M - 1];
                     if (a0 == 0.0) {  // stall: no draw is consumed
-                        for (; j <= JL; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
+                        fill = true;
                         status = CWC_TRAJ_STALLED;
                         live = false;
                     } else {
@@ -519,6 +559,11 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                     }
                 }
                 if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
+                const unsigned fm = __ballot_sync(0xffffffffu, fill);
+                if (fm) {
+                    stall_fill<S>(rp, tt, acc, fm, x, cell_base, g, j, JL, lane);
+                    if (fill) j = JL + 1;
+                }
             }
 #pragma unroll
             for (int i = 0; i < B; ++i) {
