@@ -173,6 +173,7 @@ struct WarpTables {
     const int32_t *dep_ptr;       // [M+1]
     const int2 *dep;              // (m, slot | owner lane << 24) of every m in D(mu)
     const int2 *dep16;            // the same slots for the 16-lane segment layout
+    const int4 *dep4;             // warp layout with the reactants inline: (m, slot | owner << 24, ia, ib | kind << 24)
     const int32_t *obs_ptr;       // [O+1]
     const int32_t *obs_cells;
     const int32_t *init;          // [n_cells]

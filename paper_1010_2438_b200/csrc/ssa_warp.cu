@@ -299,9 +299,10 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             // Dependency-graph update: recompute a_m for m in D(mu) only.
             unsigned dirty = 0;
             const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
-            for (int q = db + lane; q < de; q += 32) {
-                const int2 d = __ldg(wt.dep + q);
-                as[d.y & 0xffffff] = propensity(wt, xs, rates, d.x);
+            for (int q = db + lane; q < de; q += 32) {  // (reactants inline: no dependent load of rx[m])
+                const int4 d = __ldg(wt.dep4 + q);
+                as[d.y & 0xffffff] =
+                    __dmul_rn(__ldg(rates + d.x), combos(xs[d.z], xs[d.w & 0xffffff], (d.w >> 24) & 1, d.w >> 25));
                 dirty |= 1u << (d.y >> 24);
             }
             dirty = __reduce_or_sync(kFull, dirty);
