@@ -58,6 +58,7 @@ struct cwc_model_s {
     std::vector<int2> dep_slot;   // warp path: (m, slot | owner << 24) per dependency entry
     std::vector<int2> dep_slot16; // the same for 16-lane segments
     std::vector<int4> dep_slot4;  // warp layout with the dependent's reactants inline
+    std::vector<int4> dep_slot16_4;  // 16-lane segment layout with the reactants inline
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
     int max_deps = 0;
@@ -250,6 +251,12 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
         m->dep_slot16[q] = make_int2(r, (l * m->wt.Bp16 + k) | (l << 24));
     }
 
+    m->dep_slot16_4.resize(m->dep.size());
+    for (size_t q = 0; q < m->dep.size(); ++q) {
+        const ReactionDesc &rd = m->rx[m->dep[q]];
+        m->dep_slot16_4[q] = make_int4(m->dep_slot16[q].x, m->dep_slot16[q].y, rd.ia, rd.ib | (rd.kind << 24));
+    }
+
     // thread path tables
     bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
     for (size_t q = 0; ok && q < m->nu_delta.size(); ++q)
@@ -319,7 +326,7 @@ cwc_status upload(cwc_model_s *m) {
     std::vector<int2> nu2(m->nu_cell.size());
     for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
     const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
-                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_dep4 = push_bytes(blob, m->dep_slot4), o_op = push_bytes(blob, m->obs_ptr),
+                 o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_dep4 = push_bytes(blob, m->dep_slot4), o_dep16_4 = push_bytes(blob, m->dep_slot16_4), o_op = push_bytes(blob, m->obs_ptr),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
     cudaError_t e = cudaGetDevice(&m->device);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaGetDevice");
@@ -337,6 +344,7 @@ cwc_status upload(cwc_model_s *m) {
     w.dep = (const int2 *)(b + o_dep);
     w.dep16 = (const int2 *)(b + o_dep16);
     w.dep4 = (const int4 *)(b + o_dep4);
+    w.dep16_4 = (const int4 *)(b + o_dep16_4);
     w.obs_ptr = (const int32_t *)(b + o_op);
     w.obs_cells = (const int32_t *)(b + o_oc);
     w.init = (const int32_t *)(b + o_init);

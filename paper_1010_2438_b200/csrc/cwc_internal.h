@@ -174,6 +174,7 @@ struct WarpTables {
     const int2 *dep;              // (m, slot | owner lane << 24) of every m in D(mu)
     const int2 *dep16;            // the same slots for the 16-lane segment layout
     const int4 *dep4;             // warp layout with the reactants inline: (m, slot | owner << 24, ia, ib | kind << 24)
+    const int4 *dep16_4;          // the same for the 16-lane segment layout
     const int32_t *obs_ptr;       // [O+1]
     const int32_t *obs_cells;
     const int32_t *init;          // [n_cells]

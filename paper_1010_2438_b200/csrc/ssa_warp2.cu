@@ -302,9 +302,10 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         unsigned dirty = 0;
         if (fire) {
             const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
-            for (int q = db + sl; q < de; q += 16) {
-                const int2 d = __ldg(wt.dep16 + q);
-                as[d.y & 0xffffff] = prop16(wt, xs, rates, d.x);
+            for (int q = db + sl; q < de; q += 16) {  // (reactants inline: no dependent load of rx[m])
+                const int4 d = __ldg(wt.dep16_4 + q);
+                as[d.y & 0xffffff] =
+                    __dmul_rn(__ldg(rates + d.x), combos(xs[d.z], xs[d.w & 0xffffff], (d.w >> 24) & 1, d.w >> 25));
                 dirty |= 1u << (sb + (d.y >> 24));
             }
         }
