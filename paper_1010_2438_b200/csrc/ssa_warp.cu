@@ -84,6 +84,30 @@ __device__ __forceinline__ double chunk_sum(const double *ch, int B) {
     return s;
 }
 
+// Chunk sum for long chunks (B > 16: C5) as four interleaved partial sums
+// (entries k = 4i + r into partial r, each left to right), then
+// (s0 + s1) + (s2 + s3): the same additions as a serial sum but a dependent
+// chain of ~B/4 instead of B fp64 additions on the firing's critical path.
+template <int BMAX>
+__device__ __forceinline__ double chunk_sum4(const double *ch, int B) {
+    double s[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s[r] = (r < B) ? ch[r] : 0.0;
+    if constexpr (BMAX > 0) {
+#pragma unroll
+        for (int k = 4; k < BMAX; ++k)
+            if (k < B) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+    } else {
+        int k = 4;
+        for (; k + 3 < B; k += 4) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[r] = __dadd_rn(s[r], ch[k + r]);
+        }
+        for (; k < B; ++k) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+    }
+    return __dadd_rn(__dadd_rn(s[0], s[1]), __dadd_rn(s[2], s[3]));
+}
+
 // MINB: CTAs per SM the register allocation must allow (8 -> 64 registers,
 // for models whose per-warp shared memory lets 8 CTAs reside; 6 -> 80).
 // RES: resumable runs (cwc_run_*: state load/save, launch bounds); the
@@ -170,12 +194,14 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         __syncwarp();
 
         double part = 0.0;
+        constexpr bool SUM4 = (BMAX == 0 || BMAX > 16);  // long chunks: chunk_sum4, also here
         for (int k = 0; k < B; ++k) {
             const int m = lane * B + k;
             const double a = (m < M) ? propensity(wt, xs, rates, m) : 0.0;
             as[lane * Bp + k] = a;
-            part = (k == 0) ? a : __dadd_rn(part, a);
+            if (!SUM4) part = (k == 0) ? a : __dadd_rn(part, a);
         }
+        if (SUM4) part = chunk_sum4<BMAX>(as + lane * Bp, B);
         double incl = warp_incl_scan(part, lane);
         double a0 = shfl_d(incl, 31);
         double excl = __shfl_up_sync(kFull, incl, 1);
@@ -307,7 +333,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             }
             dirty = __reduce_or_sync(kFull, dirty);
             __syncwarp();
-            if ((dirty >> lane) & 1u) part = chunk_sum<BMAX>(as + lane * Bp, B);
+            if ((dirty >> lane) & 1u) part = SUM4 ? chunk_sum4<BMAX>(as + lane * Bp, B) : chunk_sum<BMAX>(as + lane * Bp, B);
             incl = warp_incl_scan(part, lane);
             a0 = shfl_d(incl, 31);
             excl = __shfl_up_sync(kFull, incl, 1);
