@@ -309,7 +309,11 @@ cwc_status cwc_run_init(cwc_model model, int64_t n_replicas, const cwc_sweep *sw
  * of trajectories that still have samples below j_stop to record (with
  * j_stop = J+1: the unfinished ones; 0 = the window, or the run, is
  * complete); the call synchronises cuda_stream to read it (n_pending may be
- * NULL: it still synchronises). */
+ * NULL: it still synchronises).  seed must be the same in every advance of a
+ * run (it keys the trajectories' Philox streams).
+ * Errors: CWC_ERR_INVALID (quantum < 0, j_stop outside [0, J+1], state too
+ * small or its header corrupt, the argument errors of cwc_simulate),
+ * CWC_ERR_CUDA. */
 cwc_status cwc_run_advance(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
                            double sample_dt, uint64_t seed, const cwc_sim_opts *opts, int64_t quantum,
                            int64_t j_stop, void *state, size_t state_bytes, void *cuda_stream,
