@@ -388,7 +388,7 @@ def simulate(model, n_replicas, t_end, sample_dt, seed, sweep=None, want_traj=Fa
 
 def simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, quantum=0, windows=None,
                        want_traj=False, force_path=CWC_PATH_AUTO, device="cuda", checkpoint=None,
-                       kernel_events=None):
+                       kernel_events=None, replica_offset=0, replicas_total=0):
     """Run through cwc_run_init / cwc_run_advance / cwc_run_stats.
 
     quantum: firings per trajectory per advance (0 = unbounded); windows:
@@ -408,6 +408,8 @@ def simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, qu
     dev = torch.device(device)
     opts = cwc_sim_opts()
     opts.force_path = int(force_path)
+    opts.replica_offset = int(replica_offset)
+    opts.replicas_total = int(replicas_total)
     out = {"firings": torch.empty(G, dtype=torch.int64, device=dev),
            "status": torch.empty(G, dtype=torch.int32, device=dev)}
     opts.out_firings = out["firings"].data_ptr()

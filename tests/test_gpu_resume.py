@@ -164,3 +164,18 @@ def test_overflow_and_stall_survive_suspension():
             res = cwc.simulate_resumable(*args, quantum=1, windows=[2, 3, 5], want_traj=True, force_path=path)
             torch.cuda.synchronize()
             _equal(one, res)
+
+
+@pytest.mark.parametrize("path", [cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP])
+def test_resumable_shard_equals_one_shot_shard(path):
+    """A resumable run of one replica shard (replica_offset / replicas_total,
+    SURVEY 8(e)) reproduces the one-shot run of the same shard."""
+    desc, sweep = w.config("C3")[0], w.mm_sweep(3, 3)
+    cfg = dict(t_end=20.0, sample_dt=0.5, n_replicas=7, seed=2)
+    model = cwc.cwc_model_create(desc)
+    args = (model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"])
+    kw = dict(sweep=sweep, want_traj=True, force_path=path, replica_offset=5, replicas_total=16)
+    one = cwc.simulate(*args, **kw)
+    res = cwc.simulate_resumable(*args, quantum=100, windows=[11, 41], **kw)
+    torch.cuda.synchronize()
+    _equal(one, res)
