@@ -154,6 +154,33 @@ def _sample_size(name):
     return {"C1": 1024, "C2": 384, "C3": 2048, "C4": 192, "C5": 12}[name]
 
 
+def _oracle_worker(a):
+    desc, sweep, cfg, g = a
+    return oracle_sample(desc, sweep, cfg, g)
+
+
+def oracle_all_cores(desc, sweep, cfg, G, name, seconds_per_core=8.0):
+    """The oracle as it stands, one process per host core over disjoint
+    strided trajectory sets (BASELINE.md §4 "all host cores" line): firings
+    of all processes / wall time of the pool."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    per = max(1, int(_sample_size(name) * seconds_per_core / 12.0))
+    n = min(G, per * cores)
+    stride = max(1, G // n)
+    gl = list(range(0, G, stride))[:n]
+    chunks = [gl[i::cores] for i in range(cores) if gl[i::cores]]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(len(chunks)) as pool:
+        res = pool.map(_oracle_worker, [(desc, sweep, cfg, c) for c in chunks])
+    dt = time.perf_counter() - t0
+    f = sum(r[0] for r in res)
+    return {"value": f / dt, "unit": "firings/s", "cores": len(chunks), "kind": "oracle",
+            "sample": "%d of %d trajectories of %s (every %d-th g) over %d processes, full t_end; %.1f s wall"
+            % (len(gl), G, name, stride, len(chunks), dt), "cpu": _cpu_model(), "host_cores": cores}
+
+
 def run_reference(args):
     rank, world, _ = _rank_env()
     if rank != 0:
@@ -177,7 +204,7 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config_block(args.config, cfg, sweep, args.gpus, "cpu-oracle"),
             "cpu_baseline": {"value": value, "unit": "firings/s", "cores": 1, "kind": "oracle", "sample": sample,
-                             "cpu": _cpu_model()},
+                             "cpu": _cpu_model(), "host_cores": os.cpu_count()},
             "e2e": {"value": value, "unit": "firings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -192,6 +219,71 @@ def _config_block(name, cfg, sweep, n_gpus, path):
             "l2": "flushed between timed steps (256 MiB write)"}
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n):
+    """`bench.py --gpus N` started without torchrun: re-exec this script
+    under torch.distributed.run with N local ranks (one per GPU, rendezvous
+    on 127.0.0.1), NCCL's communicator-init log on.  Returns the exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % n,
+           "--master-addr=127.0.0.1", "--master-port=%d" % _free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
+
+
+def comm_check(dist, device):
+    """Every rank contributes 1 to an all-reduce: the communicator really
+    spans WORLD_SIZE ranks."""
+    import torch
+    t = torch.ones(1, dtype=torch.int64, device=device)
+    dist.all_reduce(t)
+    return int(t.item()) == dist.get_world_size()
+
+
+def selftest_dist(args):
+    """CPU self-test of the launcher and the exchange step (gloo): every
+    rank checks its RANK/LOCAL_RANK/WORLD_SIZE, contributes synthetic exact
+    moments that depend on its rank (sumsq low words near 2^64 so the merge
+    must carry) and merges them with paper_1010_2438_b200.dist.allreduce_stats;
+    rank 0 prints one JSON line with what it saw."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1010_2438_b200.dist import allreduce_stats
+    rank, world, local = _rank_env()
+    dist.init_process_group("gloo")
+    ok_env = (world == args.gpus and 0 <= rank < world and local == rank)
+    n = 6
+    count = torch.full((n,), rank + 1, dtype=torch.int64)
+    s1 = torch.arange(n, dtype=torch.int64) * (rank + 1)
+    sq = torch.stack([torch.full((n,), -1 - rank, dtype=torch.int64), torch.full((n,), rank, dtype=torch.int64)], -1)
+    allreduce_stats(count, s1, sq)
+    W = world
+    want_count = W * (W + 1) // 2
+    lo = sum((2**64 - 1 - r) for r in range(W))
+    want_lo, want_hi = lo % 2**64, lo // 2**64 + sum(range(W))
+    merged_ok = (bool((count == want_count).all()) and bool((s1 == torch.arange(n) * want_count).all())
+                 and int(sq[0, 0]) % 2**64 == want_lo and int(sq[0, 1]) == want_hi)
+    ranks = torch.zeros(W, dtype=torch.int64)
+    ranks[rank] = 1 if ok_env else 0
+    dist.all_reduce(ranks)
+    nranks_ok = comm_check(dist, "cpu")
+    if rank == 0:
+        print(json.dumps({"selftest": "dist", "world_size": W, "ranks_env_ok": int(ranks.sum()) == W,
+                          "merge_exact": merged_ok, "comm_nranks_ok": nranks_ok}), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -200,8 +292,12 @@ def run_ours(args):
     from paper_1010_2438_b200.dist import allreduce_stats
 
     rank, world, local = _rank_env()
+    if world != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
+    comm_ok = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        comm_ok = comm_check(dist, torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
@@ -339,6 +435,9 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "firings/s", "h2d_bytes_per_step": 8 * P * max(M, 1),
                     "d2h_bytes_per_step": 32 * ncell},
             "gpu_launches": 2 * args.steps, "clocks": clk}
+    if comm_ok is not None:
+        line["comm"] = {"backend": "nccl", "world_size": world, "comm_nranks_ok": comm_ok,
+                        "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n = _sample_size(args.config)
         g_list = list(range(0, G, max(1, G // n)))[:n]
@@ -346,7 +445,9 @@ def run_ours(args):
         line["cpu_baseline"] = {"value": fo / dto, "unit": "firings/s", "cores": 1, "kind": "oracle",
                                 "sample": "%d of %d trajectories of %s (every %d-th g), full t_end; %.1f s"
                                 % (len(g_list), G, args.config, max(1, G // n), dto),
-                                "cpu": _cpu_model()}
+                                "cpu": _cpu_model(), "host_cores": os.cpu_count()}
+        if not args.no_all_cores:
+            line["cpu_baseline_all_cores"] = oracle_all_cores(desc, sweep, cfg, G, args.config)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -362,7 +463,13 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-all-cores", action="store_true", help="skip the all-host-cores oracle line")
+    ap.add_argument("--selftest-dist", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if args.selftest_dist:
+        return selftest_dist(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -53,6 +53,20 @@ enum { CWC_TRAJ_DONE = 0, CWC_TRAJ_STALLED = 1, CWC_TRAJ_OVERFLOW = 2, CWC_TRAJ_
 /* Which kernel runs the SSA loop. */
 enum { CWC_PATH_AUTO = -1, CWC_PATH_THREAD = 0, CWC_PATH_WARP = 1 };
 
+/* Kernel variant (cwc_sim_opts.kernel).  AUTO = the planner's
+   choice.  THREAD_WS: warp-specialised producer/consumer thread kernel;
+   THREAD: single-warp batched thread kernel; WARP2: two trajectories per
+   warp (16-lane segments, M <= 256); WARP: one trajectory per warp.  Every
+   variant computes the same trajectories (up to the traced a0-sum-order
+   class between the thread and warp families). */
+enum { CWC_KERNEL_AUTO = 0, CWC_KERNEL_THREAD_WS = 1, CWC_KERNEL_THREAD = 2, CWC_KERNEL_WARP2 = 3,
+       CWC_KERNEL_WARP = 4 };
+
+/* Where the on-line moments accumulate (cwc_sim_opts.stats_mode): per-CTA
+   shared-memory parts flushed to global memory, or one global part updated
+   with L2 reductions.  Results are identical bit for bit. */
+enum { CWC_STATS_AUTO = 0, CWC_STATS_SHARED = 1, CWC_STATS_GLOBAL = 2 };
+
 typedef struct cwc_model_s *cwc_model; /* opaque; owned by the library */
 
 /*
@@ -154,6 +168,18 @@ typedef struct {
        after the SSA kernel (kernel-only timing); NULL = not recorded */
     void *ev_kernel_begin;
     void *ev_kernel_end;
+    /* Launch-plan overrides, 0 = the library's choice (for A/B measurements
+       and tests; none changes a result bit).  kernel: CWC_KERNEL_*, must fit
+       force_path and the model (CWC_ERR_INVALID otherwise); stats_mode:
+       CWC_STATS_* (SHARED fails with CWC_ERR_INVALID if the parts do not fit
+       in shared memory); warps_per_block: warp kernels, 1..4;
+       blocks_per_sm: warp kernels' persistent grid, 1..32 (capped by
+       occupancy).  Traced runs (n_trace > 0) run the same variant as
+       untraced ones, with trace writes compiled in. */
+    int32_t kernel;
+    int32_t stats_mode;
+    int32_t warps_per_block;
+    int32_t blocks_per_sm;
 } cwc_sim_opts;
 
 /* Summary of a created model (cwc_model_info). */
@@ -288,8 +314,13 @@ cwc_status cwc_run_state_size(cwc_model model, int64_t n_replicas, const cwc_swe
 
 /* Start a run: every trajectory at (x0, t = 0, n = 0, j = 0), all live
  * (listed longest-expected-first for sweeps), statistics zeroed.  Also stores
- * the per-point rates (host expansion of sweep).  Asynchronous on
- * cuda_stream.  Errors: as cwc_simulate, CWC_ERR_INVALID for a short state. */
+ * the per-point rates (host expansion of sweep) and a fingerprint of the
+ * arguments (model tables, rates, shape, replica shard) in the state header;
+ * every later cwc_run_advance / cwc_run_stats on the state checks it
+ * (CWC_ERR_INVALID on a mismatch), and the first advance records the seed,
+ * which later advances must repeat.  Enqueued on cuda_stream; returns after
+ * the header has been written (synchronises the stream).
+ * Errors: as cwc_simulate, CWC_ERR_INVALID for a short state. */
 cwc_status cwc_run_init(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
                         double sample_dt, const cwc_sim_opts *opts, void *state, size_t state_bytes,
                         void *cuda_stream);
@@ -310,9 +341,11 @@ cwc_status cwc_run_init(cwc_model model, int64_t n_replicas, const cwc_sweep *sw
  * j_stop = J+1: the unfinished ones; 0 = the window, or the run, is
  * complete); the call synchronises cuda_stream to read it (n_pending may be
  * NULL: it still synchronises).  seed must be the same in every advance of a
- * run (it keys the trajectories' Philox streams).
+ * run (it keys the trajectories' Philox streams; checked against the seed
+ * the first advance recorded).
  * Errors: CWC_ERR_INVALID (quantum < 0, j_stop outside [0, J+1], state too
- * small or its header corrupt, the argument errors of cwc_simulate),
+ * small, its header corrupt or its fingerprint different from these
+ * arguments / seed, the argument errors of cwc_simulate),
  * CWC_ERR_CUDA. */
 cwc_status cwc_run_advance(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
                            double sample_dt, uint64_t seed, const cwc_sim_opts *opts, int64_t quantum,
@@ -321,7 +354,9 @@ cwc_status cwc_run_advance(cwc_model model, int64_t n_replicas, const cwc_sweep 
 
 /* Reduce the run's accumulators into out_stats (device, as cwc_simulate's):
  * cells of samples every trajectory has passed are final; the others hold
- * the partial sums so far.  Asynchronous on cuda_stream. */
+ * the partial sums so far.  Reads the state header first (synchronises
+ * cuda_stream; CWC_ERR_INVALID if the fingerprint does not match these
+ * arguments), then enqueues the reduction on cuda_stream. */
 cwc_status cwc_run_stats(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end,
                          double sample_dt, const cwc_sim_opts *opts, const void *state, size_t state_bytes,
                          cwc_stats out_stats, void *cuda_stream);

@@ -68,6 +68,8 @@ def _load():
         _lib.oracle_select.argtypes = [P, ctypes.c_int, ctypes.c_double]
         _lib.oracle_tau_stream.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64,
                                            ctypes.c_double, P, P]
+        _lib.oracle_tau.restype = ctypes.c_double
+        _lib.oracle_tau.argtypes = [ctypes.c_double, ctypes.c_double]
         _lib.oracle_binomial.restype = ctypes.c_int64
         _lib.oracle_binomial.argtypes = [ctypes.c_int64, ctypes.c_int64]
     return _lib
@@ -93,6 +95,11 @@ def uniforms(w):
     u2 = ctypes.c_double()
     lib.oracle_uniforms(_ptr(ww), ctypes.byref(u1), ctypes.byref(u2))
     return u1.value, u2.value
+
+
+def tau(u1, a0):
+    """The oracle's time step tau = (-log u1) / a0 (the function its loop calls)."""
+    return float(_load().oracle_tau(float(u1), float(a0)))
 
 
 def tau_stream(seed, g, n0, count, a0):

@@ -76,6 +76,13 @@ void oracle_uniforms(const uint32_t w[4], double *u1, double *u2)
     *u2 = (double)(b >> 11) * 0x1.0p-53;
 }
 
+/* tau = (-log u1) / a0: one negation, glibc log, one IEEE division
+ * (SURVEY 8(c).4).  The one place the loop forms tau. */
+double oracle_tau(double u1, double a0)
+{
+    return (-log(u1)) / a0;
+}
+
 /* The (tau, u2) pair the loop draws for firings n0 .. n0+count-1 of trajectory g
  * at a fixed total rate a0: tau = (-log u1) / a0.  Test hook. */
 void oracle_tau_stream(uint64_t seed, uint64_t g, uint64_t n0, int64_t count, double a0,
@@ -86,7 +93,7 @@ void oracle_tau_stream(uint64_t seed, uint64_t g, uint64_t n0, int64_t count, do
         draw_block(seed, g, n0 + (uint64_t)i, w);
         double u1, u2;
         oracle_uniforms(w, &u1, &u2);
-        tau_out[i] = (-log(u1)) / a0;
+        tau_out[i] = oracle_tau(u1, a0);
         u2_out[i] = u2;
     }
 }
@@ -229,7 +236,7 @@ int oracle_simulate(const oracle_model *m, int32_t n_rules, const double *rule_r
             n += 1;
             double u1, u2;
             oracle_uniforms(w, &u1, &u2);
-            double tau = (-log(u1)) / a0;
+            double tau = oracle_tau(u1, a0);
             double tn = t + tau;
             while (j <= J && (double)j * dt <= tn) {     /* samples before the event */
                 record(&rc, j, x);

@@ -14,6 +14,8 @@
 #include <cstring>
 #include <algorithm>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -65,10 +67,15 @@ struct cwc_model_s {
     int vbits = 31;   // observables are < 2^vbits (sums of int32 counts)
     bool thread_ok = false;
     ThreadTables tt{};
-    // device copies (one allocation)
-    DeviceBuf dev;
-    WarpTables wt{};
-    int device = 0;
+    WarpTables wt{};  // sizes (host); device pointers live in the per-device copies
+    // device copies of the tables, one per CUDA device the handle was used on
+    // (one allocation each), created on first use under the mutex
+    struct DevCopy {
+        DeviceBuf buf;
+        WarpTables wt{};
+    };
+    std::mutex dev_mu;
+    std::map<int, std::unique_ptr<DevCopy>> dev;
 };
 
 namespace {
@@ -318,25 +325,39 @@ size_t push_bytes(std::vector<unsigned char> &blob, const std::vector<T> &v) {
     return off;
 }
 
-cwc_status upload(cwc_model_s *m) {
+// The model's tables on the calling thread's current CUDA device: uploaded
+// there on first use (one copy per device, so one handle can serve several
+// GPUs of a process), under the handle's mutex (concurrent first calls
+// upload once).
+cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
     int ndev = 0;
     cudaError_t e0 = cudaGetDeviceCount(&ndev);
     if (e0 != cudaSuccess || ndev == 0) return fail(CWC_ERR_CUDA, "no CUDA device (there is no CPU fallback)");
+    int device = 0;
+    cudaError_t e = cudaGetDevice(&device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(m->dev_mu);
+    auto it = m->dev.find(device);
+    if (it != m->dev.end()) {
+        *out = &it->second->wt;
+        return CWC_OK;
+    }
     std::vector<unsigned char> blob;
     std::vector<int2> nu2(m->nu_cell.size());
     for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
     const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
                  o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_dep4 = push_bytes(blob, m->dep_slot4), o_dep16_4 = push_bytes(blob, m->dep_slot16_4), o_op = push_bytes(blob, m->obs_ptr),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
-    cudaError_t e = cudaGetDevice(&m->device);
-    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaGetDevice");
-    e = cudaMalloc(&m->dev.p, blob.size());
-    if (e == cudaErrorMemoryAllocation) return fail(CWC_ERR_NOMEM, "cwc_model_create: device tables");
-    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaMalloc");
-    e = cudaMemcpy(m->dev.p, blob.data(), blob.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return cuda_fail(e, "cwc_model_create: cudaMemcpy");
-    unsigned char *b = (unsigned char *)m->dev.p;
-    WarpTables &w = m->wt;
+    std::unique_ptr<cwc_model_s::DevCopy> dc(new (std::nothrow) cwc_model_s::DevCopy());
+    if (!dc) return fail(CWC_ERR_NOMEM, "host allocation");
+    e = cudaMalloc(&dc->buf.p, blob.size());
+    if (e == cudaErrorMemoryAllocation) return fail(CWC_ERR_NOMEM, "model tables: device allocation");
+    if (e != cudaSuccess) return cuda_fail(e, "model tables: cudaMalloc");
+    e = cudaMemcpy(dc->buf.p, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "model tables: cudaMemcpy");
+    unsigned char *b = (unsigned char *)dc->buf.p;
+    WarpTables &w = dc->wt;
+    w = m->wt;
     w.rx = (const ReactionDesc *)(b + o_rx);
     w.nu_ptr = (const int32_t *)(b + o_nup);
     w.nu = (const int2 *)(b + o_nu);
@@ -348,6 +369,8 @@ cwc_status upload(cwc_model_s *m) {
     w.obs_ptr = (const int32_t *)(b + o_op);
     w.obs_cells = (const int32_t *)(b + o_oc);
     w.init = (const int32_t *)(b + o_init);
+    *out = &dc->wt;
+    m->dev.emplace(device, std::move(dc));
     return CWC_OK;
 }
 
@@ -428,14 +451,35 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     const int nsm = sm_count();
 
     int force = opts ? opts->force_path : CWC_PATH_AUTO;
-    if (const char *e = env("CWC_FORCE_PATH")) force = std::atoi(e);
+    const int kern = opts ? opts->kernel : CWC_KERNEL_AUTO;
+    const int smode = opts ? opts->stats_mode : CWC_STATS_AUTO;
+    const int wpb = opts ? opts->warps_per_block : 0;
+    const int bps = opts ? opts->blocks_per_sm : 0;
+    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_WARP) return fail(CWC_ERR_INVALID, "bad kernel");
+    if (smode < CWC_STATS_AUTO || smode > CWC_STATS_GLOBAL) return fail(CWC_ERR_INVALID, "bad stats_mode");
+    if (wpb < 0 || wpb > 4) return fail(CWC_ERR_INVALID, "warps_per_block must be in [0, 4]");
+    if (bps < 0 || bps > 32) return fail(CWC_ERR_INVALID, "blocks_per_sm must be in [0, 32]");
+    if (force != CWC_PATH_AUTO && force != CWC_PATH_THREAD && force != CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "bad force_path");
+    if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD) {
+        if (force == CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
+        force = CWC_PATH_THREAD;
+    } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP) {
+        if (force == CWC_PATH_THREAD) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
+        force = CWC_PATH_WARP;
+    }
     if (force == CWC_PATH_THREAD && !m->thread_ok) return fail(CWC_ERR_INVALID, "thread path cannot run this model (too many cells/reactions/observables)");
     pl.path = (force == CWC_PATH_AUTO) ? (m->thread_ok ? CWC_PATH_THREAD : CWC_PATH_WARP) : force;
-    if (pl.path != CWC_PATH_THREAD && pl.path != CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "bad force_path");
-    int bt = opts ? opts->block_threads : 0;
-    if (const char *e = env("CWC_BLOCK_THREADS")) bt = std::atoi(e);
+    const int bt = opts ? opts->block_threads : 0;
     if (bt != 0 && (bt < 32 || bt > 256 || bt % 32)) return fail(CWC_ERR_INVALID, "block_threads must be a multiple of 32 in [32, 256]");
-    const char *smode = env("CWC_STATS_MODE");
+    // exact integer moments: every per-cell sum of observables (< 2^vbits)
+    // over all replicas of the (sharded) run must fit int64 (stage 2 and the
+    // multi-GPU merge narrow the exact sum to int64)
+    {
+        const double r_all = (opts && opts->replicas_total > 0) ? (double)opts->replicas_total : (double)n_replicas;
+        if (r_all * std::ldexp(1.0, m->vbits) >= 9.2e18)
+            return fail(CWC_ERR_INVALID, "observable sums over the replicas could exceed int64 (fewer replicas per point)");
+    }
+    if (resumable && smode == CWC_STATS_SHARED) return fail(CWC_ERR_INVALID, "resumable runs accumulate in global memory (stats_mode)");
     const size_t smem_cap = 200 * 1024;
 
     if (pl.path == CWC_PATH_THREAD) {
@@ -454,9 +498,14 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // scarce (<= 2 per SM sub-partition: C1, C2); with more (C3) the
         // single-warp kernel, whose warps carry their own draws, uses every
         // sub-partition (measured: C3 11.2 vs 11.9 ms, C2 6.4e10 vs 6.9e10)
-        const bool tracing = opts && opts->n_trace > 0;
-        bool ws = !tracing && !bt && (pl.G + 31) / 32 <= 2ll * 4 * nsm;
-        if (const char *e = env("CWC_WS")) ws = !tracing && !bt && std::atoi(e) != 0;
+        bool ws = !bt && (pl.G + 31) / 32 <= 2ll * 4 * nsm;
+        if (kern == CWC_KERNEL_THREAD_WS) {
+            if (resumable) return fail(CWC_ERR_INVALID, "resumable runs do not use the warp-specialised kernel");
+            if (bt && bt != 32 * kWsGroups) return fail(CWC_ERR_INVALID, "the warp-specialised kernel has a fixed CTA shape (block_threads)");
+            ws = true;
+        } else if (kern == CWC_KERNEL_THREAD) {
+            ws = false;
+        }
         if (resumable) ws = false;
         if (ws) T = 32 * kWsGroups;
         pl.ws = ws ? 1 : 0;
@@ -480,8 +529,11 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
         bool use_smem = smem + extra <= smem_cap &&
                         (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
-        if (smode) use_smem = std::strcmp(smode, "smem") == 0 && smem <= smem_cap;
-        if (O == 0 || resumable) use_smem = false;
+        if (smode == CWC_STATS_SHARED) {
+            if (smem + extra > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
+            use_smem = true;
+        }
+        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable) use_smem = false;
         if (use_smem) {
             pl.stats_smem = 1;
             pl.st = lay_s;
@@ -502,12 +554,16 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     } else {
         const WarpTables &w = m->wt;
         int W = bt ? std::min(bt / 32, 4) : 4;  // ssa_warp_kernel is built for <= 128 threads
-        if (const char *e = env("CWC_WARPS_PER_BLOCK")) W = std::atoi(e);
+        if (wpb) W = wpb;
         pl.warps_per_block = W;
         // two trajectories per warp (16-lane segments) when a segment's chunks
-        // stay short (M <= 256); both kernels write traces
+        // stay short (M <= 256)
         bool seg2 = w.B16 <= 16;
-        if (const char *e = env("CWC_WARP_SEG")) seg2 = w.B16 <= 16 && std::atoi(e) == 16;
+        if (kern == CWC_KERNEL_WARP2) {
+            if (!seg2) return fail(CWC_ERR_INVALID, "kernel WARP2 needs M <= 256");
+        } else if (kern == CWC_KERNEL_WARP) {
+            seg2 = false;
+        }
         pl.seg2 = seg2 ? 1 : 0;
         const size_t per_warp = seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w);
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
@@ -517,8 +573,11 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // kernel holds 8 CTAs of 4 warps per SM): crossings are rare, so the
         // global-memory parts (fire-and-forget REDs to L2) are nearly free
         bool use_smem = (stats + W * per_warp) * 8 <= 200 * 1024;
-        if (smode) use_smem = std::strcmp(smode, "smem") == 0 && stats + W * per_warp <= smem_cap;
-        if (O == 0 || resumable) use_smem = false;
+        if (smode == CWC_STATS_SHARED) {
+            if (stats + W * per_warp > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
+            use_smem = true;
+        }
+        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
         pl.st = use_smem ? lay_s : lay_g;
         pl.cells_per_part = cells;
@@ -530,7 +589,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int by_smem = (int)std::max<size_t>(1, (228 * 1024) / (pl.smem_bytes + 1024));
         const int by_threads = std::max(1, 2048 / (W * 32));
         per_sm = std::min(by_smem, by_threads);
-        if (const char *e = env("CWC_BLOCKS_PER_SM")) per_sm = std::atoi(e);
+        if (bps) per_sm = std::min(per_sm, bps);
         int64_t blocks = (int64_t)nsm * per_sm;
         blocks = std::min<int64_t>(blocks, (NL + W - 1) / W);
         pl.blocks = (int)std::max<int64_t>(1, blocks);
@@ -538,6 +597,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // a shared-memory part takes <= 2^16 trajectories (16-bit limbs); the
         // kernel caps each CTA at that, so the grid must cover G with it
         if (use_smem && (int64_t)pl.blocks * kSmemPartMaxTraj < pl.G) {
+            if (smode == CWC_STATS_SHARED) return fail(CWC_ERR_INVALID, "stats_mode SHARED: too many trajectories per CTA part");
             use_smem = false;
             pl.stats_smem = 0;
             pl.st = lay_g;
@@ -635,21 +695,21 @@ cwc_status apply_shard(RunParams &rp, const cwc_sim_opts *opts, int64_t n_replic
     return CWC_OK;
 }
 
-cudaError_t launch_ssa(const cwc_model_s *m, const Plan &pl, const RunParams &rp, cudaStream_t stream) {
+cudaError_t launch_ssa(const cwc_model_s *m, const WarpTables &wt, const Plan &pl, const RunParams &rp,
+                       cudaStream_t stream) {
     if (pl.path == CWC_PATH_THREAD)
         return launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
-    return pl.seg2 ? launch_ssa_warp2(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
-                   : launch_ssa_warp(rp, m->wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
+    return pl.seg2 ? launch_ssa_warp2(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
+                   : launch_ssa_warp(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
 }
 
 cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt, uint64_t seed,
                void *stream_, cwc_stats st, void *ws, size_t ws_bytes, const cwc_sim_opts *opts, bool host_stats,
                cwc_stats host_out) {
     if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
-    if (!m->dev.p) {  // tables go to the device on first use (host-only creation needs no GPU)
-        cwc_status su = upload(m);
-        if (su != CWC_OK) return su;
-    }
+    const WarpTables *dwt = nullptr;  // tables go to the device on first use (host-only creation needs no GPU)
+    cwc_status su = device_tables(m, &dwt);
+    if (su != CWC_OK) return su;
     Plan pl;
     cwc_status s = plan_run(m, n_replicas, sweep, t_end, dt, opts, host_stats, pl);
     if (s != CWC_OK) return s;
@@ -685,7 +745,9 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.n_parts = pl.n_parts;
     rp.traj_per_part = pl.traj_per_part;
     rp.next_traj = (unsigned long long *)(w + pl.off_counter);
-    if (const char *e = env("CWC_PROF_PTR")) rp.prof = (unsigned long long *)std::strtoull(e, nullptr, 0);  // debug hook
+#ifdef CWC_DEBUG_KNOBS  // debug builds only (tools/ws_prof.py): consumer cycle accounting buffer
+    if (const char *e = env("CWC_PROF_PTR")) rp.prof = (unsigned long long *)std::strtoull(e, nullptr, 0);
+#endif
     if (opts) {
         s = apply_shard(rp, opts, n_replicas);
         if (s != CWC_OK) return s;
@@ -723,18 +785,20 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     // measured slower on C2: a producer's fp64-heavy log stream on the same
     // sub-partition delays the consumer's fp64 chain more than a second
     // consumer does.  Kept as an experiment switch.
+#ifdef CWC_DEBUG_KNOBS
     if (pl.ws && env("CWC_WS_MIX") && std::atoi(env("CWC_WS_MIX")) != 0) {
         e = cudaMemsetAsync(w + pl.off_smctr, 0, sizeof(unsigned) * 1024, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: SM counters");
         rp.sm_ctr = (unsigned *)(w + pl.off_smctr);
     }
+#endif
     e = cudaMemsetAsync(w + pl.off_counter, 0, 16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: counter");
 
     cudaEvent_t ev0 = opts ? (cudaEvent_t)opts->ev_kernel_begin : nullptr;
     cudaEvent_t ev1 = opts ? (cudaEvent_t)opts->ev_kernel_end : nullptr;
     if (ev0 && (e = cudaEventRecord(ev0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_begin");
-    e = launch_ssa(m, pl, rp, stream);
+    e = launch_ssa(m, *dwt, pl, rp, stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: SSA kernel launch");
     if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_kernel_end");
     cwc_stats dst = st;
@@ -767,7 +831,30 @@ struct StateLayout {
     size_t hdr = 0, rates = 0, parts = 0, x = 0, t = 0, n = 0, j = 0, live0 = 0, live1 = 0, temp = 0, temp_bytes = 0,
            total = 0;
 };
-constexpr size_t kHdrLive = 0, kHdrCounter = 16, kHdrOut = 32, kHdrPending = 40, kHdrBytes = 256;
+constexpr size_t kHdrLive = 0, kHdrCounter = 16, kHdrOut = 32, kHdrPending = 40, kHdrPrint = 64, kHdrBytes = 256;
+
+// Run fingerprint at header offset kHdrPrint, written by cwc_run_init and
+// checked by every later call on the state: layout version, the plan's
+// shape, the shard, a hash of the flat model tables and of the per-point
+// rates, and the seed (recorded by the first advance, checked by the next).
+constexpr uint64_t kPrintMagic = 0x43574352554e0002ull;  // "CWCRUN" + layout version 2
+struct RunPrint {
+    uint64_t magic;
+    int64_t G, J, n_cells, M, P, O, R_total, r_off;
+    uint64_t tables_hash, rates_hash;
+    uint64_t seed, seed_set;
+};
+static_assert(kHdrPrint + sizeof(RunPrint) <= kHdrBytes, "header too small");
+
+uint64_t fnv1a(uint64_t h, const void *p, size_t n) {
+    const unsigned char *b = (const unsigned char *)p;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+    return h;
+}
+template <typename T>
+uint64_t fnv_vec(uint64_t h, const std::vector<T> &v) {
+    return fnv1a(h, v.data(), v.size() * sizeof(T));
+}
 
 StateLayout state_layout(const cwc_model_s *m, const Plan &pl) {
     StateLayout l;
@@ -799,17 +886,60 @@ StateLayout state_layout(const cwc_model_s *m, const Plan &pl) {
 }
 
 cwc_status run_prepare(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double dt,
-                       const cwc_sim_opts *opts, const void *state, size_t state_bytes, Plan &pl, StateLayout &sl) {
+                       const cwc_sim_opts *opts, const void *state, size_t state_bytes, Plan &pl, StateLayout &sl,
+                       const WarpTables **dwt) {
     if (!m) return fail(CWC_ERR_INVALID, "model is NULL");
     cwc_status s = plan_run(m, n_replicas, sweep, t_end, dt, opts, false, pl, true, -1);
     if (s != CWC_OK) return s;
     sl = state_layout(m, pl);
     if (!state) return fail(CWC_ERR_INVALID, "state is NULL");
     if (state_bytes < sl.total) return fail(CWC_ERR_INVALID, "state too small: need " + std::to_string(sl.total) + " bytes");
-    if (!m->dev.p) {
-        s = upload(m);
-        if (s != CWC_OK) return s;
-    }
+    return device_tables(m, dwt);
+}
+
+RunPrint run_print(const cwc_model_s *m, const Plan &pl, const cwc_sim_opts *opts, const std::vector<double> &rates) {
+    RunPrint f{};
+    f.magic = kPrintMagic;
+    f.G = pl.G;
+    f.J = pl.J;
+    f.n_cells = m->n_cells;
+    f.M = m->M;
+    f.P = pl.P;
+    f.O = m->n_obs;
+    f.R_total = (opts && opts->replicas_total) ? opts->replicas_total : pl.R;
+    f.r_off = opts ? opts->replica_offset : 0;
+    uint64_t h = 0xcbf29ce484222325ull;
+    h = fnv_vec(h, m->entry_rule);
+    h = fnv_vec(h, m->re_cell);
+    h = fnv_vec(h, m->re_mult);
+    h = fnv_vec(h, m->nu_cell);
+    h = fnv_vec(h, m->nu_delta);
+    h = fnv_vec(h, m->init);
+    h = fnv_vec(h, m->obs_of_cell);
+    f.tables_hash = h;
+    f.rates_hash = fnv_vec(0xcbf29ce484222325ull, rates);
+    return f;
+}
+
+// Read the state header (synchronises the stream) and check the fingerprint
+// against this call's arguments (and seed, when seed_check).
+cwc_status check_print(const cwc_model_s *m, const Plan &pl, const cwc_sim_opts *opts, const cwc_sweep *sweep,
+                       const StateLayout &sl, const unsigned char *st, cudaStream_t stream, bool seed_check,
+                       uint64_t seed, unsigned char (&hdr)[kHdrBytes], const char *who) {
+    cudaError_t e = cudaMemcpyAsync(hdr, st + sl.hdr, kHdrBytes, cudaMemcpyDeviceToHost, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+    if (e != cudaSuccess) return cuda_fail(e, (std::string(who) + ": state header").c_str());
+    RunPrint have;
+    std::memcpy(&have, hdr + kHdrPrint, sizeof(have));
+    const RunPrint want = run_print(m, pl, opts, expand_rates(m, pl, sweep));
+    if (have.magic != kPrintMagic) return fail(CWC_ERR_INVALID, std::string(who) + ": state not initialised by cwc_run_init (or corrupt)");
+    if (have.G != want.G || have.J != want.J || have.n_cells != want.n_cells || have.M != want.M || have.P != want.P ||
+        have.O != want.O || have.R_total != want.R_total || have.r_off != want.r_off ||
+        have.tables_hash != want.tables_hash || have.rates_hash != want.rates_hash)
+        return fail(CWC_ERR_INVALID, std::string(who) + ": arguments differ from the ones the state was initialised with "
+                    "(model, n_replicas, sweep, t_end, sample_dt, replica shard)");
+    if (seed_check && have.seed_set && have.seed != seed)
+        return fail(CWC_ERR_INVALID, std::string(who) + ": seed differs from the run's earlier advances");
     return CWC_OK;
 }
 
@@ -864,7 +994,8 @@ cwc_status cwc_run_init(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep,
                         const cwc_sim_opts *opts, void *state, size_t state_bytes, void *cuda_stream) {
     Plan pl;
     StateLayout sl;
-    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl);
+    const WarpTables *dwt = nullptr;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl, &dwt);
     if (s != CWC_OK) return s;
     cudaStream_t stream = (cudaStream_t)cuda_stream;
     unsigned char *st = (unsigned char *)state;
@@ -876,7 +1007,7 @@ cwc_status cwc_run_init(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep,
     // sweeps: the live list starts longest-expected-first, in groups of 32
     // (a warp of the thread path); compaction keeps that order
     const bool lpt = pl.P > 1;
-    e = launch_state_init(pl.G, m->n_cells, m->wt.init, (int32_t *)(st + sl.x), (double *)(st + sl.t),
+    e = launch_state_init(pl.G, m->n_cells, dwt->init, (int32_t *)(st + sl.x), (double *)(st + sl.t),
                           (int64_t *)(st + sl.n), (int32_t *)(st + sl.j), lpt ? nullptr : (int64_t *)(st + sl.live0),
                           stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: state");
@@ -891,8 +1022,15 @@ cwc_status cwc_run_init(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep,
         e = cudaMemcpyAsync(st + sl.live0, live.data(), sizeof(int64_t) * live.size(), cudaMemcpyHostToDevice, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: live list");
     }
-    const int64_t hdr[2] = {pl.G, 0};
-    e = cudaMemcpyAsync(st + sl.hdr + kHdrLive, hdr, sizeof(hdr), cudaMemcpyHostToDevice, stream);
+    // header: live count, dispatch counter, fingerprint (the call then
+    // synchronises: the host header must outlive the copy)
+    unsigned char hdr[kHdrBytes] = {};
+    const int64_t live_n[2] = {pl.G, 0};
+    std::memcpy(hdr + kHdrLive, live_n, sizeof(live_n));
+    const RunPrint f = run_print(m, pl, opts, rates);
+    std::memcpy(hdr + kHdrPrint, &f, sizeof(f));
+    e = cudaMemcpyAsync(st + sl.hdr, hdr, kHdrBytes, cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
     if (e != cudaSuccess) return cuda_fail(e, "cwc_run_init: header");
     return CWC_OK;
 }
@@ -902,18 +1040,32 @@ cwc_status cwc_run_advance(cwc_model m, int64_t n_replicas, const cwc_sweep *swe
                            size_t state_bytes, void *cuda_stream, int64_t *n_pending) {
     Plan pl0;
     StateLayout sl;
-    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl0, sl);
+    const WarpTables *dwt = nullptr;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl0, sl, &dwt);
     if (s != CWC_OK) return s;
     if (quantum < 0) return fail(CWC_ERR_INVALID, "quantum must be >= 0");
     if (j_stop == 0) j_stop = (int64_t)pl0.J + 1;
     if (j_stop < 1 || j_stop > (int64_t)pl0.J + 1) return fail(CWC_ERR_INVALID, "j_stop must be in [1, J+1] (or 0)");
     cudaStream_t stream = (cudaStream_t)cuda_stream;
     unsigned char *st = (unsigned char *)state;
+    unsigned char hdr[kHdrBytes];
+    s = check_print(m, pl0, opts, sweep, sl, st, stream, true, seed, hdr, "cwc_run_advance");
+    if (s != CWC_OK) return s;
     int64_t nl = 0;
-    cudaError_t e = cudaMemcpyAsync(&nl, st + sl.hdr + kHdrLive, sizeof(int64_t), cudaMemcpyDeviceToHost, stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: live count");
+    std::memcpy(&nl, hdr + kHdrLive, sizeof(nl));
     if (nl < 0 || nl > pl0.G) return fail(CWC_ERR_INVALID, "state header corrupt (live count out of range)");
+    cudaError_t e = cudaSuccess;
+    {
+        RunPrint f;
+        std::memcpy(&f, hdr + kHdrPrint, sizeof(f));
+        if (!f.seed_set) {  // the first advance records the run's seed
+            f.seed = seed;
+            f.seed_set = 1;
+            e = cudaMemcpyAsync(st + sl.hdr + kHdrPrint, &f, sizeof(f), cudaMemcpyHostToDevice, stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+            if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: header");
+        }
+    }
     int64_t n_out = 0;
     if (nl > 0) {
         Plan pl;
@@ -929,7 +1081,7 @@ cwc_status cwc_run_advance(cwc_model m, int64_t n_replicas, const cwc_sweep *swe
         cudaEvent_t ev0 = opts ? (cudaEvent_t)opts->ev_kernel_begin : nullptr;
         cudaEvent_t ev1 = opts ? (cudaEvent_t)opts->ev_kernel_end : nullptr;
         if (ev0 && (e = cudaEventRecord(ev0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_run_advance: ev_kernel_begin");
-        e = launch_ssa(m, pl, rp, stream);
+        e = launch_ssa(m, *dwt, pl, rp, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_run_advance: SSA kernel launch");
         if (ev1 && (e = cudaEventRecord(ev1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_run_advance: ev_kernel_end");
         // compaction: live1 = unfinished entries of live0 (order kept)
@@ -968,7 +1120,12 @@ cwc_status cwc_run_stats(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep
                          void *cuda_stream) {
     Plan pl;
     StateLayout sl;
-    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl);
+    const WarpTables *dwt = nullptr;
+    cwc_status s = run_prepare(m, n_replicas, sweep, t_end, sample_dt, opts, state, state_bytes, pl, sl, &dwt);
+    if (s != CWC_OK) return s;
+    unsigned char hdr[kHdrBytes];
+    s = check_print(m, pl, opts, sweep, sl, (const unsigned char *)state, (cudaStream_t)cuda_stream, false, 0, hdr,
+                    "cwc_run_stats");
     if (s != CWC_OK) return s;
     if (pl.n_stat_cells == 0) return CWC_OK;
     if (!out_stats.count || !out_stats.sum || !out_stats.sumsq) return fail(CWC_ERR_INVALID, "stats pointers are NULL");

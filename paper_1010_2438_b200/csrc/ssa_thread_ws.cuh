@@ -40,10 +40,10 @@ namespace cwc {
 // Hand-off counters live in shared memory; accesses use the shared state
 // space (LDS/STS, not generic loads).  prod: release store by the producer
 // (its ring writes are ordered before it), acquire load by the consumer.
-// cons/done: plain (relaxed) stores by the consumer -- the ring loads they
-// release have already returned their values (the consumer used them), so no
-// later producer store can affect them; a release here would be a MEMBAR
-// that waits for the consumer's in-flight statistics atomics in L2.
+// cons: release store by the consumer (its ring loads are ordered before it
+// under the PTX memory model, so the producer, which acquires cons, can
+// never overwrite a slot the consumer has not read yet), acquire load by
+// the producer.  done: relaxed (it orders nothing: the producer only stops).
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
             }
             if (prof) { c1 = clock64(); pc[3] += c1 - c0; c0 = c1; }
             // release consumed slots (the slot reads above are ordered before it)
-            st_relaxed(cons + lane, (unsigned)n);
+            st_release(cons + lane, (unsigned)n);
             if (in_range && !live) st_relaxed(done + lane, 1u);
             asm volatile("bar.warp.sync -1;" ::: "memory");
         }

@@ -345,7 +345,9 @@ cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int bloc
     const int x_bytes = align16b(4ll * (wt.n_cells + 1));
     const int per_seg = (int)(warp2_smem_per_warp(wt) / 2);
     bool small = (size_t)smem_bytes * 8 <= (size_t)220 * 1024 && warps_per_block <= 4;
+#ifdef CWC_DEBUG_KNOBS
     if (const char *e = std::getenv("CWC_WARP2_MINB")) small = std::atoi(e) == 8 && small;  // experiment switch
+#endif
     auto k = (rp.n_trace > 0) ? (small ? ssa_warp2_kernel<8, true> : ssa_warp2_kernel<6, true>)
                               : (small ? ssa_warp2_kernel<8, false> : ssa_warp2_kernel<6, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);

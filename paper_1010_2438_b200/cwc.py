@@ -21,6 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libcwcsim.so")
 CWC_OK, CWC_ERR_INVALID, CWC_ERR_UNSUPPORTED, CWC_ERR_CUDA, CWC_ERR_NOMEM = 0, -1, -2, -3, -4
 CWC_TRAJ_DONE, CWC_TRAJ_STALLED, CWC_TRAJ_OVERFLOW, CWC_TRAJ_RUNNING = 0, 1, 2, 3
 CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
+CWC_KERNEL_AUTO, CWC_KERNEL_THREAD_WS, CWC_KERNEL_THREAD, CWC_KERNEL_WARP2, CWC_KERNEL_WARP = 0, 1, 2, 3, 4
+CWC_STATS_AUTO, CWC_STATS_SHARED, CWC_STATS_GLOBAL = 0, 1, 2
 
 EXPORTED = ["cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
             "cwc_simulate_workspace_size", "cwc_simulate", "cwc_simulate_host", "cwc_simulate_host_workspace_size",
@@ -57,7 +59,8 @@ class cwc_stats(ctypes.Structure):
 class cwc_sim_opts(ctypes.Structure):
     _fields_ = [("out_traj", P), ("out_firings", P), ("out_status", P), ("trace_g", P), ("n_trace", I32),
                 ("trace_cap", I64), ("trace_buf", P), ("trace_len", P), ("force_path", I32), ("block_threads", I32),
-                ("replica_offset", I64), ("replicas_total", I64), ("ev_kernel_begin", P), ("ev_kernel_end", P)]
+                ("replica_offset", I64), ("replicas_total", I64), ("ev_kernel_begin", P), ("ev_kernel_end", P),
+                ("kernel", I32), ("stats_mode", I32), ("warps_per_block", I32), ("blocks_per_sm", I32)]
 
 
 class cwc_model_info(ctypes.Structure):
@@ -319,15 +322,33 @@ def cwc_run_stats(model, n_replicas, sweep, t_end, sample_dt, state, stats, stre
 # convenience: allocate torch outputs and run (the calls above do the work)
 # ---------------------------------------------------------------------------
 
+def _plan_opts(opts, kernel=CWC_KERNEL_AUTO, stats_mode=CWC_STATS_AUTO, warps_per_block=0, blocks_per_sm=0):
+    opts.kernel = int(kernel)
+    opts.stats_mode = int(stats_mode)
+    opts.warps_per_block = int(warps_per_block)
+    opts.blocks_per_sm = int(blocks_per_sm)
+
+
 def simulate(model, n_replicas, t_end, sample_dt, seed, sweep=None, want_traj=False, want_firings=True,
              trace_g=(), trace_cap=0, force_path=CWC_PATH_AUTO, block_threads=0, device="cuda", stream=None,
-             finalize=False, replica_offset=0, replicas_total=0, kernel_events=None, buffers=None):
+             finalize=False, replica_offset=0, replicas_total=0, kernel_events=None, buffers=None, **plan):
     """Allocate outputs (or reuse `buffers` from a previous call) and run
-    cwc_simulate once.  kernel_events: (begin, end) torch.cuda.Event pair
-    recorded around the SSA kernel."""
+    cwc_simulate once on `device` (made current for the call).
+    kernel_events: (begin, end) torch.cuda.Event pair recorded around the
+    SSA kernel.  plan: kernel / stats_mode / warps_per_block / blocks_per_sm
+    overrides of cwc_sim_opts."""
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("cwc: no CUDA device (there is no CPU fallback)")
+    with torch.cuda.device(torch.device(device)):
+        return _simulate(torch, model, n_replicas, t_end, sample_dt, seed, sweep, want_traj, want_firings, trace_g,
+                         trace_cap, force_path, block_threads, device, stream, finalize, replica_offset,
+                         replicas_total, kernel_events, buffers, plan)
+
+
+def _simulate(torch, model, n_replicas, t_end, sample_dt, seed, sweep, want_traj, want_firings, trace_g, trace_cap,
+              force_path, block_threads, device, stream, finalize, replica_offset, replicas_total, kernel_events,
+              buffers, plan):
     P_ = len(sweep["values"]) if sweep is not None else 1
     G = P_ * int(n_replicas)
     J1 = n_samples(t_end, sample_dt)
@@ -343,6 +364,7 @@ def simulate(model, n_replicas, t_end, sample_dt, seed, sweep=None, want_traj=Fa
     opts = cwc_sim_opts()
     opts.force_path = int(force_path)
     opts.block_threads = int(block_threads)
+    _plan_opts(opts, **plan)
     opts.replica_offset = int(replica_offset)
     opts.replicas_total = int(replicas_total)
     if kernel_events is not None:
@@ -388,7 +410,17 @@ def simulate(model, n_replicas, t_end, sample_dt, seed, sweep=None, want_traj=Fa
 
 def simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, quantum=0, windows=None,
                        want_traj=False, force_path=CWC_PATH_AUTO, device="cuda", checkpoint=None,
-                       kernel_events=None, replica_offset=0, replicas_total=0):
+                       kernel_events=None, replica_offset=0, replicas_total=0, **plan):
+    import torch
+    with torch.cuda.device(torch.device(device)):
+        return _simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep, quantum, windows, want_traj,
+                                   force_path, device, checkpoint, kernel_events, replica_offset, replicas_total,
+                                   **plan)
+
+
+def _simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, quantum=0, windows=None,
+                        want_traj=False, force_path=CWC_PATH_AUTO, device="cuda", checkpoint=None,
+                        kernel_events=None, replica_offset=0, replicas_total=0, **plan):
     """Run through cwc_run_init / cwc_run_advance / cwc_run_stats.
 
     quantum: firings per trajectory per advance (0 = unbounded); windows:
@@ -408,6 +440,7 @@ def simulate_resumable(model, n_replicas, t_end, sample_dt, seed, sweep=None, qu
     dev = torch.device(device)
     opts = cwc_sim_opts()
     opts.force_path = int(force_path)
+    _plan_opts(opts, **plan)
     opts.replica_offset = int(replica_offset)
     opts.replicas_total = int(replicas_total)
     out = {"firings": torch.empty(G, dtype=torch.int64, device=dev),

@@ -177,3 +177,59 @@ def test_run_state_size_and_errors():
     with pytest.raises(cwc.CwcError) as ei:
         cwc.cwc_run_state_size(m, 16, None, 1.0, 0.1, opts)
     assert ei.value.status == cwc.CWC_ERR_INVALID
+
+
+def _opts(**kw):
+    o = cwc.cwc_sim_opts()
+    o.force_path = cwc.CWC_PATH_AUTO
+    for k, v in kw.items():
+        setattr(o, k, v)
+    return o
+
+
+def test_plan_override_validation():
+    """cwc_sim_opts plan overrides (kernel, stats_mode, warps_per_block,
+    blocks_per_sm) are validated; nothing is read from the environment."""
+    c2 = cwc.cwc_model_create(w.config("C2")[0])
+    c5 = cwc.cwc_model_create(w.config("C5")[0])
+    ok = [dict(kernel=cwc.CWC_KERNEL_THREAD_WS), dict(kernel=cwc.CWC_KERNEL_THREAD), dict(kernel=cwc.CWC_KERNEL_WARP2),
+          dict(kernel=cwc.CWC_KERNEL_WARP), dict(stats_mode=cwc.CWC_STATS_GLOBAL), dict(stats_mode=cwc.CWC_STATS_SHARED),
+          dict(kernel=cwc.CWC_KERNEL_WARP, warps_per_block=2, blocks_per_sm=3)]
+    for kw in ok:
+        assert cwc.cwc_simulate_workspace_size(c2, 64, None, 1.0, 0.1, _opts(**kw)) > 0, kw
+    bad = [(c2, dict(kernel=7)), (c2, dict(kernel=-1)), (c2, dict(stats_mode=3)), (c2, dict(warps_per_block=5)),
+           (c2, dict(warps_per_block=-1)), (c2, dict(blocks_per_sm=33)), (c2, dict(force_path=5)),
+           (c2, dict(kernel=cwc.CWC_KERNEL_WARP, force_path=cwc.CWC_PATH_THREAD)),
+           (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, force_path=cwc.CWC_PATH_WARP)),
+           (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, block_threads=64)),
+           (c5, dict(kernel=cwc.CWC_KERNEL_THREAD)),      # 264 cells: no thread path
+           (c5, dict(kernel=cwc.CWC_KERNEL_WARP2))]       # M = 1172 > 256
+    for m, kw in bad:
+        with pytest.raises(cwc.CwcError) as ei:
+            cwc.cwc_simulate_workspace_size(m, 64, None, 1.0, 0.1, _opts(**kw))
+        assert ei.value.status == cwc.CWC_ERR_INVALID, kw
+    # resumable runs: no warp-specialised kernel, no shared-memory parts
+    for kw in (dict(kernel=cwc.CWC_KERNEL_THREAD_WS), dict(stats_mode=cwc.CWC_STATS_SHARED)):
+        with pytest.raises(cwc.CwcError) as ei:
+            cwc.cwc_run_state_size(c2, 64, None, 1.0, 0.1, _opts(**kw))
+        assert ei.value.status == cwc.CWC_ERR_INVALID, kw
+
+
+def test_environment_does_not_change_the_plan(monkeypatch):
+    """The round-1 experiment variables are no longer read by release builds."""
+    m = cwc.cwc_model_create(w.config("C4")[0])
+    a = cwc.cwc_simulate_workspace_size(m, 64, None, 1.0, 0.1)
+    for k, v in [("CWC_STATS_MODE", "smem"), ("CWC_WARP_SEG", "32"), ("CWC_WARPS_PER_BLOCK", "0"),
+                 ("CWC_BLOCKS_PER_SM", "1"), ("CWC_FORCE_PATH", "0"), ("CWC_WS", "1"), ("CWC_PROF_PTR", "0x10")]:
+        monkeypatch.setenv(k, v)
+    assert cwc.cwc_simulate_workspace_size(m, 64, None, 1.0, 0.1) == a
+
+
+def test_int64_moment_bound():
+    """Per-cell observable sums over all replicas must fit int64:
+    a run whose replicas could overflow them is refused."""
+    m = cwc.cwc_model_create(w.config("C5")[0])   # observables < 2^36
+    assert cwc.cwc_simulate_workspace_size(m, 8192, None, 1.0, 0.1) > 0
+    with pytest.raises(cwc.CwcError) as ei:
+        cwc.cwc_simulate_workspace_size(m, 16, None, 1.0, 0.1, _opts(replicas_total=2**28))
+    assert ei.value.status == cwc.CWC_ERR_INVALID

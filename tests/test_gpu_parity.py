@@ -120,20 +120,18 @@ SMALL = [
 ]
 
 
-KERNELS = [("thread", cwc.CWC_PATH_THREAD, {}),                     # warp-specialised thread kernel
+KERNELS = [("thread", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS}),  # warp-specialised thread kernel
            ("thread1", cwc.CWC_PATH_THREAD, {"block_threads": 64}),  # single-warp batched thread kernel
            ("warp", cwc.CWC_PATH_WARP, {}),                           # two trajectories per warp (M <= 256)
-           ("warp32", cwc.CWC_PATH_WARP, {"CWC_WARP_SEG": "32"})]     # one trajectory per warp
+           ("warp32", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP})]  # one trajectory per warp
 
 
 @pytest.mark.parametrize("name,make,cfg", SMALL, ids=[s[0] for s in SMALL])
 @pytest.mark.parametrize("kname,path,kw", KERNELS, ids=[k[0] for k in KERNELS])
-def test_small_parity_full_oracle(name, make, cfg, kname, path, kw, monkeypatch):
+def test_small_parity_full_oracle(name, make, cfg, kname, path, kw):
     kw = dict(kw)
     if name in ("cwc130", "cwc260", "lv16") and path == cwc.CWC_PATH_THREAD:
         pytest.skip("more than 8 cells: warp path only")
-    for k in [k for k in kw if k.startswith("CWC_")]:
-        monkeypatch.setenv(k, kw.pop(k))
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
     gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path, **kw)
@@ -182,16 +180,15 @@ def test_launch_shape_does_not_change_results(bt):
         assert torch.equal(ref[k], got[k]), k
 
 
-@pytest.mark.parametrize("mode", ["smem", "global"])
-def test_stats_modes_agree(mode, monkeypatch):
+@pytest.mark.parametrize("mode", [cwc.CWC_STATS_SHARED, cwc.CWC_STATS_GLOBAL])
+def test_stats_modes_agree(mode):
     desc, sweep, _ = w.config("C3")
     sweep = w.mm_sweep(6, 6)
     cfg = dict(t_end=20.0, sample_dt=0.5, n_replicas=40, seed=1)
     model = cwc.cwc_model_create(desc)
     ref = _gpu(model, cfg, sweep)
-    monkeypatch.setenv("CWC_STATS_MODE", mode)
     for path in (cwc.CWC_PATH_THREAD, cwc.CWC_PATH_WARP):
-        got = _gpu(model, cfg, sweep, force_path=path)
+        got = _gpu(model, cfg, sweep, force_path=path, stats_mode=mode)
         for k in ("count", "sum", "sumsq"):
             assert torch.equal(ref[k], got[k]), (mode, path, k)
 
@@ -208,12 +205,11 @@ def test_finalize_matches_oracle_moments():
         assert np.all(np.abs(g - wv) <= 1e-9 * np.maximum(np.abs(g), np.abs(wv)))
 
 
-@pytest.mark.parametrize("seg", ["16", "32"])
-def test_trace_warp_paths_against_oracle(seg, monkeypatch):
+@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_WARP2, cwc.CWC_KERNEL_WARP])
+def test_trace_warp_paths_against_oracle(kern):
     """The warp kernels' per-firing traces (n, a0, tau, t', mu) against the
     oracle's: identical or differing only by the classified ulp-level
     reasons (sum order of a0 / the chunk prefixes, log ulp), never BUG."""
-    monkeypatch.setenv("CWC_WARP_SEG", seg)
     desc = w.random_network_model(seed=5, n_species=8, n_reactions=24)
     cfg = dict(t_end=0.2, sample_dt=0.02, n_replicas=20, seed=3)
     model = cwc.cwc_model_create(desc)
@@ -308,7 +304,7 @@ def test_host_output_api_equals_device_output():
 
 
 @pytest.mark.parametrize("name,R,t_end", [("C2", 40000, 0.05), ("C3", 700, 5.0)])
-def test_thread_kernels_agree_bitwise_multiwave(name, R, t_end, monkeypatch):
+def test_thread_kernels_agree_bitwise_multiwave(name, R, t_end):
     """The warp-specialised and the single-warp thread kernels compute the same
     trajectories bit for bit, also when the grid needs several waves of CTAs
     (C2: 40000 replicas; C3: 4096 points x 700 replicas, longest-first
@@ -316,9 +312,7 @@ def test_thread_kernels_agree_bitwise_multiwave(name, R, t_end, monkeypatch):
     desc, sweep, _ = w.config(name)
     cfg = dict(t_end=t_end, sample_dt=t_end / 5, n_replicas=R, seed=9)
     model = cwc.cwc_model_create(desc)
-    monkeypatch.setenv("CWC_WS", "1")
-    a = _gpu(model, cfg, sweep)
-    monkeypatch.setenv("CWC_WS", "0")
-    b = _gpu(model, cfg, sweep)
+    a = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD_WS)
+    b = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD)
     for k in ("count", "sum", "sumsq", "firings", "status"):
         assert torch.equal(a[k], b[k]), k

@@ -33,9 +33,9 @@ CASES = [
     ("cwc130", lambda: (w.small_cwc_model(130, 2), None), dict(t_end=0.3, sample_dt=0.05, n_replicas=40, seed=4)),
 ]
 
-KERNELS = [("thread", cwc.CWC_PATH_THREAD, None),
-           ("warp", cwc.CWC_PATH_WARP, None),      # two trajectories per warp (M <= 256)
-           ("warp32", cwc.CWC_PATH_WARP, "32")]    # one trajectory per warp
+KERNELS = [("thread", cwc.CWC_PATH_THREAD, cwc.CWC_KERNEL_AUTO),
+           ("warp", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_AUTO),   # two trajectories per warp (M <= 256)
+           ("warp32", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP)]  # one trajectory per warp
 
 
 def _schedules(J1):
@@ -50,20 +50,18 @@ def _equal(a, b, keys=("count", "sum", "sumsq", "firings", "status", "traj")):
 
 
 @pytest.mark.parametrize("name,make,cfg", CASES, ids=[c[0] for c in CASES])
-@pytest.mark.parametrize("kname,path,seg", KERNELS, ids=[k[0] for k in KERNELS])
-def test_resumable_equals_one_shot(name, make, cfg, kname, path, seg, monkeypatch):
+@pytest.mark.parametrize("kname,path,kern", KERNELS, ids=[k[0] for k in KERNELS])
+def test_resumable_equals_one_shot(name, make, cfg, kname, path, kern):
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
     if path == cwc.CWC_PATH_THREAD and not model.info.thread_path_ok:
         pytest.skip("more than 8 cells: warp path only")
-    if seg:
-        monkeypatch.setenv("CWC_WARP_SEG", seg)
     args = (model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"])
-    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path)
+    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path, kernel=kern)
     torch.cuda.synchronize()
     J1 = one["J1"]
     for sname, sch in _schedules(J1):
-        res = cwc.simulate_resumable(*args, sweep=sweep, want_traj=True, force_path=path, **sch)
+        res = cwc.simulate_resumable(*args, sweep=sweep, want_traj=True, force_path=path, kernel=kern, **sch)
         torch.cuda.synchronize()
         _equal(one, res)
         assert res["live"][-1] == 0
@@ -96,7 +94,7 @@ def test_checkpoint_through_host_memory(path):
     cfg = dict(t_end=20.0, sample_dt=0.5, n_replicas=20, seed=11)
     model = cwc.cwc_model_create(desc)
     args = (model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"])
-    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path)
+    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path, kernel=kern)
     torch.cuda.synchronize()
     saved = {}
 

@@ -80,9 +80,14 @@ def test_uniform_edges():
 
 
 def test_tau_examples_spec():
-    # u = e^-1, r = 2 -> tau = 0.5 ; u = 1 -> tau = 0
-    assert abs((-math.log(math.exp(-1.0))) / 2.0 - 0.5) < 1e-15
-    assert (-math.log(1.0)) / 5.0 == 0.0
+    # S:203-205 through the oracle's own tau (the function its loop calls):
+    # u = e^-1, r = 2 -> tau = 0.5 (within 1 ulp: e^-1 is rounded); u = 1 -> tau = 0
+    assert abs(oracle.tau(math.exp(-1.0), 2.0) - 0.5) <= 2.0**-53
+    assert oracle.tau(1.0, 5.0) == 0.0
+    # the smallest u1 the conversion produces (2^-53): tau = 53 ln 2 / a0
+    assert abs(oracle.tau(2.0**-53, 1.0) - 53 * math.log(2.0)) <= 2 * 2.0**-47
+    # tau scales as 1 / a0 (one IEEE division of the same -log u1)
+    assert oracle.tau(0.3, 1.0) / 4.0 == oracle.tau(0.3, 4.0)
 
 
 def test_exponential_moments_from_philox_stream():
@@ -102,14 +107,23 @@ def test_u2_uniformity_chi2():
     assert chi2 < 100.0  # df = 49, p ~ 3e-5
 
 
-def test_tau_stream_is_the_philox_block_formula():
-    # the stream helper uses block (n, g) with the documented conversion
-    tau, u2 = oracle.tau_stream(5, 11, 100, 3, 4.0)
-    for i in range(3):
+def test_tau_stream_is_exact_within_one_ulp():
+    # the stream's tau of block (n, g) against the exact value -ln(u1) / a0
+    # (mpmath, 60 digits), u1 from the uniform conversion pinned above.
+    # glibc's log is within 1 ulp of E = -ln u1, i.e. relative error < 2^-52,
+    # and the division rounds once more (2^-53 relative): |tau - exact| <
+    # 1.5 * 2^-52 * exact.  (A dropped negation, a reciprocal multiply
+    # instead of the division, or log1p(-u) would all fail this.)
+    import mpmath
+    mpmath.mp.dps = 60
+    a0 = 3.7
+    tau, u2 = oracle.tau_stream(5, 11, 100, 400, a0)
+    for i in range(400):
         w = oracle.philox4x32_10([100 + i, 0, 11, 0], [5, 0])
         u1, v2 = oracle.uniforms(w)
         assert u2[i] == v2
-        assert tau[i] == (-math.log(u1)) / 4.0
+        exact = -mpmath.log(mpmath.mpf(u1)) / mpmath.mpf(a0)
+        assert abs(mpmath.mpf(tau[i]) - exact) <= mpmath.mpf(1.5) * mpmath.mpf(2) ** -52 * exact, i
 
 
 def _kat():

@@ -17,6 +17,9 @@ model = cwc.cwc_model_create(desc)
 R, T, dt = cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"]
 
 
+KERNEL = cwc.CWC_KERNEL_AUTO
+
+
 def timed(sw, reps=R):
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     ev[0].record()
@@ -24,7 +27,7 @@ def timed(sw, reps=R):
     out = None
     ms = []
     for _ in range(3):
-        out = cwc.simulate(model, reps, T, dt, 1, sweep=sw, kernel_events=ev)
+        out = cwc.simulate(model, reps, T, dt, 1, sweep=sw, kernel_events=ev, kernel=KERNEL)
         torch.cuda.synchronize()
         ms.append(ev[0].elapsed_time(ev[1]))
     return min(ms), out
@@ -42,13 +45,13 @@ for k in (1, 2, 8, 32, 128, 512):
     print(json.dumps(dict(case="top%d" % k, points=k, kernel_ms=ms, max_firings=f, ns_per_firing=ms * 1e6 / f)))
 
 if os.environ.get("WS_TOO"):
-    os.environ["CWC_WS"] = "1"
+    KERNEL = cwc.CWC_KERNEL_THREAD_WS
     for k in (8, 128, 512, 1024, 4096):
         sub = {"rules": sweep["rules"], "values": [sweep["values"][i] for i in order[:k]]}
         ms, out = timed(sub)
         f = int(out["firings"].max())
         print(json.dumps(dict(case="ws_top%d" % k, points=k, kernel_ms=ms, max_firings=f, ns_per_firing=ms * 1e6 / f)))
-    os.environ["CWC_WS"] = "0"
+    KERNEL = cwc.CWC_KERNEL_THREAD
     for k in (1024, 4096):
         sub = {"rules": sweep["rules"], "values": [sweep["values"][i] for i in order[:k]]}
         ms, out = timed(sub)

@@ -32,25 +32,22 @@ for n in (2, 4, 8, 16, 32):
     model = cwc.cwc_model_create(wl.lotka_volterra_chain(n))
     kernels = []
     if model.info.thread_path_ok:
-        kernels.append(("thread_ws", cwc.CWC_PATH_THREAD, None))
+        kernels.append(("thread_ws", cwc.CWC_PATH_THREAD, cwc.CWC_KERNEL_THREAD_WS))
     if (model.info.n_reactions + 15) // 16 <= 16:
-        kernels.append(("warp2", cwc.CWC_PATH_WARP, "16"))
-    kernels.append(("warp", cwc.CWC_PATH_WARP, "32"))
-    for name, path, seg in kernels:
-        if seg:
-            os.environ["CWC_WARP_SEG"] = seg
+        kernels.append(("warp2", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP2))
+    kernels.append(("warp", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP))
+    for name, path, kern in kernels:
         best, buf = None, None
         for k in range(4):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            out = cwc.simulate(model, a.replicas, a.t_end, 0.01, 1, force_path=path, buffers=buf)
+            out = cwc.simulate(model, a.replicas, a.t_end, 0.01, 1, force_path=path, kernel=kern, buffers=buf)
             e1.record()
             torch.cuda.synchronize()
             buf = out
             ms = e0.elapsed_time(e1)
             if k > 0:
                 best = ms if best is None else min(best, ms)
-        os.environ.pop("CWC_WARP_SEG", None)
         f = int(out["firings"].sum().item())
         line = {"n_species": n, "reactions": model.info.n_reactions, "kernel": name, "replicas": a.replicas,
                 "t_end": a.t_end, "firings": f, "ms": best, "firings_per_s": f / best * 1e3}
