@@ -525,7 +525,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const size_t smem = (size_t)stat_bytes(lay_s, cells);
         // beyond the statistics part: the draw ring + staging of the
         // warp-specialised CTA, or the record staging of each warp
-        const size_t extra = ws ? kWsRingBytes : (size_t)(T / 32) * kStageLL * sizeof(long long);
+        const size_t extra = (ws ? kWsRingBytes : (size_t)(T / 32) * kStageLL * sizeof(long long)) + kNegLogSmemBytes;
         const int64_t resident_needed = (blocks + nsm - 1) / nsm;
         bool use_smem = smem + extra <= smem_cap &&
                         (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;

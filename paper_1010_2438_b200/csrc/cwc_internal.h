@@ -62,6 +62,13 @@ constexpr size_t kWsGroupBytes = (size_t)2 * kWsRing * 32 * sizeof(double) +
 // staging longs per warp: per record its first cell, its dump row, its counts (int32)
 constexpr long long kStageLL = (long long)kWsStage * (2 + kThreadMaxCells / 2);
 constexpr size_t kWsRingBytes = kWsGroups * ((kWsGroupBytes + 15) & ~(size_t)15);  // per CTA
+// shared-memory copy of the -log reduction table (device_common.cuh,
+// neglog_table.h) in the thread kernels: {T, L_hi} pairs then L_lo
+struct NegLogSmem {
+    double2 tl[129];
+    double lo[129];
+};
+constexpr size_t kNegLogSmemBytes = (sizeof(NegLogSmem) + 15) & ~(size_t)15;
 constexpr long long kSmemPartMaxTraj = 1ll << 16;  // trajectories per shared-memory part (16-bit limbs)
 __host__ __device__ __forceinline__ long long stat_cells_round(long long n) { return (n + 3) & ~3ll; }
 // Layout for observables of at most vbits bits (v < 2^vbits, v^2 < 2^(2 vbits)).

@@ -133,6 +133,13 @@ __device__ __forceinline__ bool apply_nu(const int (&x)[S], unsigned long long n
     return wrapped;
 }
 
+// Per-firing values of a speculative firing, kept for the divergence trace
+// (TRACE builds only; n, a0, tau, t', mu as the oracle's trace records).
+struct FireRec {
+    double a0, tau, tn;
+    int mu;
+};
+
 // One speculative firing of the fast batch: propensities, a0, tau and the
 // selection, update applied at once; returns whether the firing was "plain"
 // (fast division valid -- a0 > 0 and in range --, no sample crossed, no count
@@ -168,27 +175,44 @@ struct FastChain {
     __device__ __forceinline__ bool step(const ThreadTables &tt, const Gather<S, M> &gt, const double (&c)[M],
                                          int (&x)[S], double &t, double E, double U, double t_next) {
         bool cross1;
-        return step2(tt, gt, c, x, t, E, U, t_next, t_next, cross1);
+        FireRec fr;
+        return step2<false>(tt, gt, c, x, t, E, U, t_next, t_next, cross1, fr);
     }
 
     // As step(); additionally cross1 = the firing crossed exactly one sample
-    // time (t_next <= t + tau < t_next2) and is otherwise plain.
+    // time (t_next <= t + tau < t_next2) and is otherwise plain.  TR: also
+    // fill fr with the firing's (a0, tau, t', mu) for the trace (the same
+    // arithmetic; mu = the number of cumulative sums <= target).
+    template <bool TR>
     __device__ __forceinline__ bool step2(const ThreadTables &tt, const Gather<S, M> &gt, const double (&c)[M],
                                           int (&x)[S], double &t, double E, double U, double t_next, double t_next2,
-                                          bool &cross1) {
+                                          bool &cross1, FireRec &fr) {
         double cum[M];
         if constexpr (OPND) {
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const double a = __dmul_rn(ch[m], __ll2double_rn((long long)A[m] * (long long)Bo[m]));
+                // RN(A Bo) as one fp64 product of the exact operands: equals
+                // the int64 product rounded once (|A Bo| < 2^62), without the
+                // quarter-rate int64 -> fp64 conversion on the state chain
+                const double a = __dmul_rn(ch[m], __dmul_rn(i2d_exact(A[m]), i2d_exact(Bo[m])));
                 cum[m] = (m == 0) ? a : __dadd_rn(cum[m - 1], a);
             }
         } else {
             cumulative(tt, gt, x, c, cum);
         }
         const double a0 = cum[M - 1];
-        const double tn = __dadd_rn(t, div_fast(E, a0));
+        const double tau = div_fast(E, a0);
+        const double tn = __dadd_rn(t, tau);
         const double target = __dmul_rn(U, a0);
+        if (TR) {
+            int k = 0;
+#pragma unroll
+            for (int m = 0; m + 1 < M; ++m) k += (cum[m] <= target) ? 1 : 0;
+            fr.a0 = a0;
+            fr.tau = tau;
+            fr.tn = tn;
+            fr.mu = k;
+        }
         unsigned long long nu, op[NW];
         if constexpr (COMB) {
             unsigned long long cw = tt.comb_pack[0];
@@ -326,6 +350,9 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
     int *st_x = (int *)(st_row + kWsStage);                   // [kWsStage][kThreadMaxCells] pre-event counts
     const int lane = threadIdx.x & 31;
     int stage_n = 0;  // warp-uniform
+    // the CTA's copy of the -log table (after the staging areas of its warps)
+    NegLogSmem *ltab = (NegLogSmem *)(smem + stats_part_bytes + (T >> 5) * kStageLL * (long long)sizeof(long long));
+    neglog_smem_fill(ltab, threadIdx.x, (int)T);
 
     StatAcc acc;
     long long p_base = 0;
@@ -335,12 +362,12 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         const long long n16 = stat_bytes(rp.st, rp.cells_per_part) / 16;
         for (long long i = threadIdx.x; i < n16; i += T) z[i] = make_uint4(0, 0, 0, 0);
         p_base = g0 / rp.R;
-        __syncthreads();
     } else {
         acc = stat_view((unsigned char *)rp.parts + (cta % rp.n_parts) * stat_bytes(rp.st, rp.cells_per_part),
                         rp.cells_per_part, rp.st);
     }
 
+    __syncthreads();  // statistics part zeroed, table staged
     // Lanes past the last trajectory stay in the warp-uniform loop as idle
     // lanes (their loads use a valid trajectory id; they never record).
     const bool in_range = slot < rp.n_launch;
@@ -421,27 +448,31 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
             const bool jok = j < JL;
             const double t_next0 = t_next, t_next20 = t_next2;
             const double t_next3 = __dmul_rn(__ll2double_rn(j + 2), rp.dt);
+            FireRec fr[B];
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
                 for (int ph = 0; ph < 4; ++ph)
-                    if ((ph * B) / 4 == k) pipe.phase(ph, rp.seed, En, Un);
+                    if ((ph * B) / 4 == k) pipe.phase(ph, rp.seed, ltab, En, Un);
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
                 bool cross1;
-                const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
+                const bool plain = fc.template step2<TRACE>(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1, fr[k]);
                 const bool take = cross1 && !rec && jok;
                 rec = rec || take;
                 krec = take ? k : krec;
                 t_next = take ? t_next2 : t_next;
                 t_next2 = take ? t_next3 : t_next2;
-                // TRACE builds take every firing through the exact path below
-                // (it writes the trace)
-                bad |= (!TRACE && (plain || take)) ? 0u : (1u << k);
+                bad |= (plain || take) ? 0u : (1u << k);
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
+            if (TRACE && live) {  // trace records of the committed speculative firings
+#pragma unroll
+                for (int k = 0; k < B; ++k)
+                    if (k < used) trace_rec(n0 + k, fr[k].a0, fr[k].tau, fr[k].tn, fr[k].mu);
+            }
             if (rec && krec >= used) {  // the crossing firing was rolled back
                 rec = false;
                 t_next = t_next0;
@@ -519,12 +550,12 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                             int mu;
                             const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
                             int xn[S];
+                            trace_rec(n, a0, tau, tn, mu);  // (the oracle records an overflowing firing too)
                             if (apply_nu(x, nu, xn)) {  // a count would leave int32: freeze + fill
                                 for (; j <= JL; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
                                 status = CWC_TRAJ_OVERFLOW;
                                 live = false;
                             } else {
-                                trace_rec(n, a0, tau, tn, mu);
 #pragma unroll
                                 for (int s = 0; s < S; ++s) x[s] = xn[s];
                                 t = tn;
@@ -606,15 +637,15 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
     }
 }
 
-template <int S, int M>
+template <int S, int M, bool TRACE>
 __global__ void ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt);
 
 template <int S, int M>
 cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, size_t smem, cudaStream_t st,
                       bool trace) {
     const long long blocks = (rp.n_launch + threads - 1) / threads;
-    if (rp.ws && !trace) {  // warp-specialised: 32 trajectories per 2-warp CTA (ssa_thread_ws.cuh)
-        auto k = ssa_thread_ws_kernel<S, M>;
+    if (rp.ws) {  // warp-specialised: 32 trajectories per 2-warp CTA (ssa_thread_ws.cuh)
+        auto k = trace ? ssa_thread_ws_kernel<S, M, true> : ssa_thread_ws_kernel<S, M, false>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 32 * (1 + kWsProducers) * kWsGroups, smem, st>>>(rp, tt);

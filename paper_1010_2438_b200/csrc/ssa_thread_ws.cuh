@@ -57,7 +57,11 @@ __device__ __forceinline__ void st_relaxed(unsigned *p, unsigned v) {
     asm volatile("st.relaxed.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
 }
 
-template <int S, int M>
+// TRACE: the same kernel with per-firing trace records (n, a0, tau, t', mu)
+// of the trajectories in rp.trace_g written by the consumer (divergence
+// tracer: the traced run is the warp-specialised kernel, fast batches
+// included).
+template <int S, int M, bool TRACE>
 __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <= 12 && CWC_WS_MINB / kWsGroups / kWsProducers > 1) ? CWC_WS_MINB / kWsGroups / kWsProducers : 1) ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt) {
     // consumer batch B; one producer warp per group computes rounds of PW
     // draws (round r = draws [r PW, r PW + PW) of each of its trajectories)
@@ -113,6 +117,8 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
     long long *st_row = st_cell + kWsStage;            // [kWsStage] its trajectory sample row (out_traj)
     int *st_x = (int *)(st_row + kWsStage);            // [kWsStage][kThreadMaxCells] its pre-event counts
 
+    NegLogSmem *ltab = (NegLogSmem *)(smem + stats_bytes + kWsRingBytes);  // the CTA's -log table
+    neglog_smem_fill(ltab, threadIdx.x, blockDim.x);
     StatAcc acc;
     long long p_base = 0;
     if (rp.stats_smem) {
@@ -150,7 +156,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
                 double Ew[PW], Uw[PW];
                 pipe.start(gk, p);
 #pragma unroll
-                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.seed, Ew, Uw);
+                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.seed, ltab, Ew, Uw);
                 if (room) {
 #pragma unroll
                     for (int i = 0; i < PW; ++i) {
@@ -180,6 +186,18 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
         FastChain<S, M> fc;
         fc.rates(tt, c);
         fc.load(tt, x);
+
+        int tslot = -1;
+        long long tn_rec = 0;
+        if (TRACE && in_range)
+            for (int i = 0; i < rp.n_trace; ++i)
+                if (rp.trace_g[i] == g) tslot = i;
+        auto trace_rec = [&](unsigned long long n_, double a0_, double tau_, double tn_, int mu_) {
+            if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
+                double *r = rp.trace_buf + ((long long)tslot * rp.trace_cap + tn_rec++) * 5;
+                r[0] = (double)n_; r[1] = a0_; r[2] = tau_; r[3] = tn_; r[4] = (double)mu_;
+            }
+        };
 
         int stage_n = 0;  // staged records (warp-uniform)
         unsigned long long avail = 0;  // draws of this trajectory known to be published
@@ -244,13 +262,14 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
             const bool jok = j < J;
             const double t_next0 = t_next, t_next20 = t_next2;
             const double t_next3 = __dmul_rn(__ll2double_rn(j + 2), rp.dt);
+            FireRec fr[B];
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
                 tsnap[k] = t;
                 bool cross1;
-                const bool plain = fc.step2(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1);
+                const bool plain = fc.template step2<TRACE>(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1, fr[k]);
                 const bool take = cross1 && !rec && jok;
                 rec = rec || take;
                 krec = take ? k : krec;
@@ -260,6 +279,11 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
             }
             if (!live) bad = 1u;
             const int used = (bad == 0u) ? B : __ffs(bad) - 1;
+            if (TRACE && live) {  // trace records of the committed speculative firings
+#pragma unroll
+                for (int k = 0; k < B; ++k)
+                    if (k < used) trace_rec(n + k, fr[k].a0, fr[k].tau, fr[k].tn, fr[k].mu);
+            }
             if (rec && krec >= used) {  // the crossing firing was rolled back
                 rec = false;
                 t_next = t_next0;
@@ -331,14 +355,16 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
                             ++j;
                         }
                         if (j > J) {  // horizon reached: drawn, not applied
+                            trace_rec(n, a0, tau, tn, -1);
                             status = CWC_TRAJ_DONE;
                             live = false;
                         } else {
                             t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
                             t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
                             int mu;
-                            const unsigned long long nu = select_nu<M, false>(tt, cum, __dmul_rn(u2, a0), mu);
+                            const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
                             int xn[S];
+                            trace_rec(n, a0, tau, tn, mu);
                             if (apply_nu(x, nu, xn)) {  // a count would leave int32: freeze + fill
                                 for (; j <= J; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
                                 status = CWC_TRAJ_OVERFLOW;
@@ -371,6 +397,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
         if (in_range) {
             if (rp.out_firings) rp.out_firings[g] = firings;
             if (rp.out_status) rp.out_status[g] = status;
+            if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
         }
     }
 

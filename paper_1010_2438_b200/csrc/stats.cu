@@ -159,13 +159,20 @@ cudaError_t launch_philox_blocks(uint64_t seed, const int64_t *g, const int64_t 
 }
 
 // ---- draw / division hooks (the SSA kernels' own device functions) ------------
+// the thread kernels' draw pipeline (shared-memory table, four phases)
 __global__ void draws_kernel(uint64_t seed, const int64_t *g, const int64_t *n, long long count, double *E,
                              double *u2) {
+    __shared__ NegLogSmem tab;
+    neglog_smem_fill(&tab, threadIdx.x, blockDim.x);
+    __syncthreads();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
-        double e, u;
-        block_to_draws(philox_block(seed, (uint64_t)g[i], (uint64_t)n[i]), e, u);
-        E[i] = e;
-        u2[i] = u;
+        DrawPipe<1> pipe;
+        double e[1], u[1];
+        pipe.start((uint64_t)g[i], (uint64_t)n[i]);
+#pragma unroll
+        for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, seed, &tab, e, u);
+        E[i] = e[0];
+        u2[i] = u[0];
     }
 }
 
@@ -175,7 +182,7 @@ __global__ void block_draws_kernel(const uint32_t *w, long long count, double *u
         block_uniforms(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3], a, b);
         u1[i] = a;
         u2[i] = b;
-        E[i] = neg_log_unit(a);
+        E[i] = neg_log_v(block_v1(w[4 * i], w[4 * i + 1]));  // the warp kernels' refill path (table through L1)
     }
 }
 

@@ -91,7 +91,8 @@ def test_draws_match_oracle_and_are_accurate():
     assert np.array_equal(U.view(np.int64), ou.view(np.int64))
     d = _ulps(E, oe)
     assert d.max() <= 1
-    assert (d == 0).mean() >= 0.98, (d == 0).mean()
+    # table-driven log: <= 0.5 ulp + 2^-60 (tools/logtable), glibc ~0.52 ulp
+    assert (d == 0).mean() >= 0.995, (d == 0).mean()
     # accuracy against the correctly rounded value on a subsample
     mpmath = pytest.importorskip("mpmath")
     mpmath.mp.prec = 200
@@ -105,7 +106,7 @@ def test_draws_match_oracle_and_are_accurate():
         ex = -mpmath.log(mpmath.mpf(u1))
         ulp = mpmath.mpf(2) ** (mpmath.floor(mpmath.log(ex, 2)) - 52)
         worst = max(worst, float(abs(mpmath.mpf(float(E[i])) - ex) / ulp))
-    assert worst < 1.0, worst
+    assert worst < 0.51, worst
 
 
 def test_uniform_conversion_edges_match_oracle():

@@ -94,7 +94,7 @@ def test_checkpoint_through_host_memory(path):
     cfg = dict(t_end=20.0, sample_dt=0.5, n_replicas=20, seed=11)
     model = cwc.cwc_model_create(desc)
     args = (model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"])
-    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path, kernel=kern)
+    one = cwc.simulate(*args, sweep=sweep, want_traj=True, force_path=path)
     torch.cuda.synchronize()
     saved = {}
 
