@@ -15,8 +15,11 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libcwcsim.so")
+# CWC_BUILD_TAG=<tag>: an experiment variant (objects in build_<tag>/, library
+# libcwcsim_<tag>.so; tools/variant_run.py loads it); the product build has no tag
+_TAG = os.environ.get("CWC_BUILD_TAG", "")
+OBJ = os.path.join(HERE, "build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(HERE, "libcwcsim" + ("_" + _TAG if _TAG else "") + ".so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -49,8 +49,9 @@ def _assert_moments_equal_dump(gpu, P, R):
     assert torch.equal(gpu["sumsq"][..., 0], (t * t).sum(dim=1))
 
 
-def _check_parity(desc, model, cfg, sweep, gpu, g_list, force_path, warp_path):
-    """Compare sampled trajectories with the oracle; trace every mismatch."""
+def _check_parity(desc, model, cfg, sweep, gpu, g_list, force_path, warp_path, **kw):
+    """Compare trajectories with the oracle; trace every mismatch with the
+    same kernel variant (kw: the run's plan overrides)."""
     ora = oracle.simulate(desc, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep,
                           g_list=g_list, want_stats=False)
     gt = gpu["traj"][torch.as_tensor(np.asarray(g_list), device="cuda")].cpu().numpy()
@@ -58,10 +59,12 @@ def _check_parity(desc, model, cfg, sweep, gpu, g_list, force_path, warp_path):
     gs = gpu["status"][torch.as_tensor(np.asarray(g_list), device="cuda")].cpu().numpy()
     same = np.array([(gt[i] == ora["traj"][i]).all() for i in range(len(g_list))])
     same &= (gf == ora["firings"]) | ~same
-    bad = [g_list[i] for i in np.nonzero(~same)[0]]
-    report = trace_mismatches(model, desc, sweep, cfg, bad, warp_path, force_path) if bad else []
+    bad_i = list(np.nonzero(~same)[0])
+    report = trace_mismatches(model, desc, sweep, cfg, [g_list[i] for i in bad_i], warp_path, force_path,
+                              gpu_rows=[gt[i] for i in bad_i], ora_rows=[ora["traj"][i] for i in bad_i],
+                              **kw) if bad_i else []
     for rec in report:
-        assert rec[1] != "BUG", rec
+        assert rec[1] not in ("BUG", "identical-trace"), rec
     assert same.mean() >= MIN_MATCH, (same.mean(), report)
     matched = np.nonzero(same)[0]
     assert (gf[matched] == ora["firings"][matched]).all()
@@ -137,7 +140,8 @@ def test_small_parity_full_oracle(name, make, cfg, kname, path, kw):
     gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path, **kw)
     P = gpu["n_points"]
     G = P * cfg["n_replicas"]
-    same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, list(range(G)), path, path == cwc.CWC_PATH_WARP)
+    same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, list(range(G)), path, path == cwc.CWC_PATH_WARP,
+                                      **kw)
     # moments: GPU on-line stats == reduction of the GPU's own dump (exact)
     _assert_moments_equal_dump(gpu, P, cfg["n_replicas"])
     if same.all():  # and == oracle's own on-line moments
@@ -213,7 +217,7 @@ def test_trace_warp_paths_against_oracle(kern):
     desc = w.random_network_model(seed=5, n_species=8, n_reactions=24)
     cfg = dict(t_end=0.2, sample_dt=0.02, n_replicas=20, seed=3)
     model = cwc.cwc_model_create(desc)
-    rep = trace_mismatches(model, desc, None, cfg, [0, 7, 19], True, cwc.CWC_PATH_WARP)
+    rep = trace_mismatches(model, desc, None, cfg, [0, 7, 19], True, cwc.CWC_PATH_WARP, kernel=kern)
     for g, cat, idx, detail in rep:
         assert cat in ("identical-trace", "log-ulp", "a0-sum-order", "select-order"), (g, cat, idx, detail)
 
@@ -227,38 +231,24 @@ def test_trace_equals_oracle_trace_thread_path():
         assert cat in ("identical-trace", "log-ulp"), (g, cat, idx, detail)
 
 
-# ---------------------------------------------------------------------------
-# full BASELINE configs, bench launch shape, oracle-sampled trajectories
-# ---------------------------------------------------------------------------
-
-FULL = [("C1", 1), ("C2", 512), ("C3", 1024), ("C4", 2048), ("C5", 2048)]
-
-
-@pytest.mark.parametrize("name,stride", FULL, ids=[f[0] for f in FULL])
-def test_full_config_sampled_parity(name, stride):
-    desc, sweep, cfg = w.config(name)
+@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_THREAD_WS, cwc.CWC_KERNEL_THREAD])
+def test_traced_thread_kernels_equal_untraced_and_each_other(kern):
+    """Trace writes compiled into a thread kernel change nothing it computes,
+    and both thread kernels (warp-specialised and single-warp, fast batches
+    included) write the same per-firing records."""
+    desc, _, _ = w.config("C2")
+    cfg = dict(t_end=0.3, sample_dt=0.01, n_replicas=96, seed=4)
     model = cwc.cwc_model_create(desc)
-    warp = model.info.path == cwc.CWC_PATH_WARP
-    gpu = _gpu(model, cfg, sweep, want_traj=True)
-    bench_like = _gpu(model, cfg, sweep, want_firings=False)  # the exact call bench.py times
-    for k in ("count", "sum", "sumsq"):
-        assert torch.equal(gpu[k], bench_like[k]), k
-    P = gpu["n_points"]
-    G = P * cfg["n_replicas"]
-    # MM trajectories that convert all substrate stall legitimately (a0 = 0)
-    assert np.isin(gpu["status"].cpu().numpy(), [cwc.CWC_TRAJ_DONE, cwc.CWC_TRAJ_STALLED]).all()
-    # exact on-line moments == reduction of the dump (every trajectory)
-    _assert_moments_equal_dump(gpu, P, cfg["n_replicas"])
-    # sampled trajectories vs the oracle (first, last, ragged stride)
-    g_list = sorted(set(list(range(0, G, stride)) + [G - 1]))
-    same, report, ora = _check_parity(desc, model, cfg, sweep, gpu, g_list, cwc.CWC_PATH_AUTO, warp)
-    # moments over the matched sample, mean / variance per sample time within 1e-9
-    idx = np.nonzero(same)[0]
-    a = gpu["traj"][torch.as_tensor(np.asarray(g_list)[idx], device="cuda")].cpu().numpy().astype(np.float64)
-    b = ora["traj"][idx].astype(np.float64)
-    assert np.allclose(a.mean(axis=0), b.mean(axis=0), rtol=1e-9, atol=0)
-    if len(idx) > 1:
-        assert np.allclose(a.var(axis=0, ddof=1), b.var(axis=0, ddof=1), rtol=1e-9, atol=1e-12)
+    args = (model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"])
+    plain = _gpu(model, cfg, kernel=kern)
+    tr = cwc.simulate(*args, trace_g=[0, 33, 95], trace_cap=20000, kernel=kern)
+    ref = cwc.simulate(*args, trace_g=[0, 33, 95], trace_cap=20000, kernel=cwc.CWC_KERNEL_THREAD_WS)
+    torch.cuda.synchronize()
+    for k in ("count", "sum", "sumsq", "firings", "status"):
+        assert torch.equal(plain[k], tr[k]), k
+    assert torch.equal(tr["trace_len"], ref["trace_len"])
+    assert (tr["trace_len"].cpu() == tr["firings"][[0, 33, 95]].cpu() + 1).all()  # + the final drawn block
+    assert torch.equal(tr["trace"], ref["trace"])
 
 
 @pytest.mark.parametrize("name", ["C2", "C4"])

@@ -20,9 +20,9 @@
 constexpr int ITERS = 2048;
 constexpr int CH = 8;
 
-enum Op { DFMA, DADD, DMUL, RCP64, I2F64, IMAD, IMADHI, LOP3, IADD3, FFMA, SHFL, LDS, N_OPS };
+enum Op { DFMA, DADD, DMUL, RCP64, I2F64, IMAD, IMADHI, LOP3, IADD3, FFMA, SHFL, LDS, IMADW, FLO, I2F64S32, N_OPS };
 static const char *names[N_OPS] = {"dfma", "dadd", "dmul", "mufu_rcp64h", "i2f_f64_u64", "imad", "imad_hi", "lop3",
-                                   "iadd3", "ffma", "shfl", "lds"};
+                                   "iadd3", "ffma", "shfl", "lds", "imad_wide_u32", "flo_clz", "i2f_f64_s32"};
 
 template <int OP, int C>
 __device__ __forceinline__ void body(double (&d)[C], uint32_t (&u)[C], float (&f)[C], double a, double b,
@@ -41,10 +41,20 @@ __device__ __forceinline__ void body(double (&d)[C], uint32_t (&u)[C], float (&f
         if (OP == IMAD) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(u[c]) : "r"(ia), "r"(ib));
         if (OP == IMADHI) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(u[c]) : "r"(ia));
         if (OP == LOP3) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(u[c]) : "r"(ia), "r"(ib));
-        if (OP == IADD3) asm volatile("add.u32 %0, %0, %1;" : "+r"(u[c]) : "r"(ia));
+        if (OP == IADD3) asm volatile("add.u32 %0, %0, %1;\n\tadd.u32 %0, %0, %2;" : "+r"(u[c]) : "r"(ia), "r"(ib));
         if (OP == FFMA) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(f[c]) : "f"((float)a), "f"((float)b));
         if (OP == SHFL) u[c] = __shfl_xor_sync(0xffffffffu, u[c], 1 + (c & 3));
         if (OP == LDS) d[c] = sm[(__double2loint(d[c]) & 255) + c];
+        if (OP == IMADW) {
+            unsigned long long p;
+            asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(u[c]), "r"(ia));
+            u[c] = (uint32_t)(p >> 32) ^ (uint32_t)p;
+        }
+        if (OP == FLO) u[c] = __clz(u[c]) + ia;
+        if (OP == I2F64S32) {
+            asm volatile("cvt.rn.f64.s32 %0, %1;" : "=d"(d[c]) : "r"(u[c]));
+            u[c] = (uint32_t)__double2hiint(d[c]);
+        }
     }
 }
 
@@ -118,6 +128,9 @@ int main() {
     if (run<FFMA>(nsm, cyc, sink, tp[FFMA], lt[FFMA])) return 1;
     if (run<SHFL>(nsm, cyc, sink, tp[SHFL], lt[SHFL])) return 1;
     if (run<LDS>(nsm, cyc, sink, tp[LDS], lt[LDS])) return 1;
+    if (run<IMADW>(nsm, cyc, sink, tp[IMADW], lt[IMADW])) return 1;
+    if (run<FLO>(nsm, cyc, sink, tp[FLO], lt[FLO])) return 1;
+    if (run<I2F64S32>(nsm, cyc, sink, tp[I2F64S32], lt[I2F64S32])) return 1;
     printf("{\"sms\": %d, \"clock_rate_khz\": %d, \"unit\": \"warp instructions per SM per cycle (throughput); "
            "cycles per dependent instruction (latency)\", \"ops\": {", nsm, clk);
     for (int i = 0; i < N_OPS; ++i)
