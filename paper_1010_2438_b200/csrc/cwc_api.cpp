@@ -491,14 +491,14 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // refills SMs as warps finish; the thread path is latency-bound, so
         // nothing is gained from larger CTAs
         int T = bt ? bt : 32;
-        // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories;
-        // ssa_thread_ws.cuh); the single-warp kernel serves traced runs and
-        // explicit block sizes
-        // warp-specialised producer/consumer CTAs while trajectory warps are
-        // scarce (<= 2 per SM sub-partition: C1, C2); with more (C3) the
-        // single-warp kernel, whose warps carry their own draws, uses every
-        // sub-partition (measured: C3 11.2 vs 11.9 ms, C2 6.4e10 vs 6.9e10)
-        bool ws = !bt && (pl.G + 31) / 32 <= 2ll * 4 * nsm;
+        // warp-specialised producer/consumer CTAs (2 warps per 32 trajectories,
+        // ssa_thread_ws.cuh) while at most two of them
+        // share an SM (their consumer and producer warps then own their
+        // sub-partitions: C1); beyond that the single-warp kernel, whose
+        // warps carry their own draws, is faster (measured with the
+        // table-driven log: C2 at 16384 replicas 8.58e10 vs 8.41e10
+        // firings/s; one lone CTA 274 vs 355 cycles per firing)
+        bool ws = !bt && (pl.G + 31) / 32 <= 2ll * nsm;
         if (kern == CWC_KERNEL_THREAD_WS) {
             if (resumable) return fail(CWC_ERR_INVALID, "resumable runs do not use the warp-specialised kernel");
             if (bt && bt != 32 * kWsGroups) return fail(CWC_ERR_INVALID, "the warp-specialised kernel has a fixed CTA shape (block_threads)");

@@ -323,9 +323,12 @@ __device__ __forceinline__ void staged_record(const RunParams &rp, const ThreadT
     }
 }
 
+#ifndef CWC_TB_SMALL  // speculative batch length for M <= 8 (experiment knob)
+#define CWC_TB_SMALL 4
+#endif
 template <int M>
 struct ThreadBatch {
-    static constexpr int B = (M <= 8) ? 4 : (M <= 16 ? 2 : 1);
+    static constexpr int B = (M <= 8) ? CWC_TB_SMALL : (M <= 16 ? 2 : 1);
 };
 
 // RES: resumable runs (cwc_run_*: state load/save, launch bounds); the
