@@ -61,6 +61,9 @@ struct cwc_model_s {
     std::vector<int2> dep_slot16; // the same for 16-lane segments
     std::vector<int4> dep_slot4;  // warp layout with the dependent's reactants inline
     std::vector<int4> dep_slot16_4;  // 16-lane segment layout with the reactants inline
+    // warp kernels' per-mu tables (WarpTables.hdr / nuw / depw16 / depw32)
+    std::vector<int4> wseg_hdr, wseg_dep16, wseg_dep32;
+    std::vector<int2> wseg_nu;
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
     int max_deps = 0;
@@ -80,7 +83,9 @@ struct cwc_model_s {
 
 namespace {
 
-bool finite_pos(double v) { return std::isfinite(v) && v > 0.0; }
+// rates are finite and >= 2^-1021 (the smallest normal fp64 number times 2):
+// the kernels pre-halve A + A rates, which is exact only in the normal range
+bool finite_pos(double v) { return std::isfinite(v) && v >= 0x1.0p-1021; }
 
 cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
     if (!d) return fail(CWC_ERR_INVALID, "desc is NULL");
@@ -117,7 +122,7 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
     m->n_obs = d->n_obs;
     m->rule_rate.assign(d->rate, d->rate + R);
     for (int r = 0; r < R; ++r) {
-        if (!finite_pos(d->rate[r])) return fail(CWC_ERR_INVALID, "rate must be finite and > 0 (rule " + std::to_string(r) + ")");
+        if (!finite_pos(d->rate[r])) return fail(CWC_ERR_INVALID, "rate must be finite and >= 2^-1021 (rule " + std::to_string(r) + ")");
         if (d->rule_label[r] < 0 || d->rule_label[r] >= NT) return fail(CWC_ERR_INVALID, "rule_label out of range (rule " + std::to_string(r) + ")");
         if (d->rule_child_label[r] < -1 || d->rule_child_label[r] >= NT)
             return fail(CWC_ERR_INVALID, "rule_child_label out of range (rule " + std::to_string(r) + ")");
@@ -264,6 +269,32 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
         m->dep_slot16_4[q] = make_int4(m->dep_slot16[q].x, m->dep_slot16[q].y, rd.ia, rd.ib | (rd.kind << 24));
     }
 
+    // warp kernels' per-mu tables: byte offsets (x: 4 bytes per cell, a: 8
+    // bytes per slot of the lane-chunk layout, rates: 8 bytes per reaction),
+    // the owner lane and the A + A flag packed as documented in WarpTables
+    if ((long long)ncell * 4 + 4 >= (1ll << 31) || (long long)M * 8 >= (1ll << 26))
+        return fail(CWC_ERR_UNSUPPORTED, "model too large for the warp kernels' tables");
+    {
+        m->wseg_hdr.resize(M);
+        for (int mu = 0; mu < M; ++mu)
+            m->wseg_hdr[mu] = make_int4(m->nu_ptr[mu], m->nu_ptr[mu + 1] - m->nu_ptr[mu], m->dep_ptr[mu],
+                                        m->dep_ptr[mu + 1] - m->dep_ptr[mu]);
+        m->wseg_nu.resize(m->nu_cell.size());
+        for (size_t q = 0; q < m->nu_cell.size(); ++q) m->wseg_nu[q] = make_int2(4 * m->nu_cell[q], m->nu_delta[q]);
+        for (int segw : {16, 32}) {
+            const int Bs = segw == 16 ? m->wt.B16 : m->wt.B;
+            const int Bps = Bs | 1;  // chunk stride (ssa_warp2.cu / ssa_warp.cu)
+            std::vector<int4> &out = segw == 16 ? m->wseg_dep16 : m->wseg_dep32;
+            out.resize(m->dep.size());
+            for (size_t q = 0; q < m->dep.size(); ++q) {
+                const int r = m->dep[q], l = r / Bs, k = r - l * Bs;
+                const ReactionDesc &rd = m->rx[r];
+                const unsigned w = (unsigned)(8 * r) | ((unsigned)(l & 31) << 26) | ((unsigned)(rd.kind & 1) << 31);
+                out[q] = make_int4(8 * (l * Bps + k), 4 * rd.ia, 4 * rd.ib, (int)w);
+            }
+        }
+    }
+
     // thread path tables
     bool ok = ncell <= kThreadMaxCells && M <= kThreadMaxReactions && m->n_obs <= kThreadMaxObs;
     for (size_t q = 0; ok && q < m->nu_delta.size(); ++q)
@@ -347,6 +378,8 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
     for (size_t q = 0; q < nu2.size(); ++q) nu2[q] = make_int2(m->nu_cell[q], m->nu_delta[q]);
     const size_t o_rx = push_bytes(blob, m->rx), o_nup = push_bytes(blob, m->nu_ptr), o_nu = push_bytes(blob, nu2),
                  o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_dep4 = push_bytes(blob, m->dep_slot4), o_dep16_4 = push_bytes(blob, m->dep_slot16_4), o_op = push_bytes(blob, m->obs_ptr),
+                 o_whdr = push_bytes(blob, m->wseg_hdr), o_wnu = push_bytes(blob, m->wseg_nu),
+                 o_wd16 = push_bytes(blob, m->wseg_dep16), o_wd32 = push_bytes(blob, m->wseg_dep32),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
     std::unique_ptr<cwc_model_s::DevCopy> dc(new (std::nothrow) cwc_model_s::DevCopy());
     if (!dc) return fail(CWC_ERR_NOMEM, "host allocation");
@@ -369,6 +402,10 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
     w.obs_ptr = (const int32_t *)(b + o_op);
     w.obs_cells = (const int32_t *)(b + o_oc);
     w.init = (const int32_t *)(b + o_init);
+    w.hdr = (const int4 *)(b + o_whdr);
+    w.nuw = (const int2 *)(b + o_wnu);
+    w.depw16 = (const int4 *)(b + o_wd16);
+    w.depw32 = (const int4 *)(b + o_wd32);
     *out = &dc->wt;
     m->dev.emplace(device, std::move(dc));
     return CWC_OK;
@@ -435,7 +472,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         for (int i = 0; i < sweep->n_swept; ++i)
             if (sweep->rule[i] < 0 || sweep->rule[i] >= m->n_rules) return fail(CWC_ERR_INVALID, "sweep rule id out of range");
         for (long long i = 0; i < (long long)sweep->n_points * sweep->n_swept; ++i)
-            if (!finite_pos(sweep->value[i])) return fail(CWC_ERR_INVALID, "sweep value must be finite and > 0");
+            if (!finite_pos(sweep->value[i])) return fail(CWC_ERR_INVALID, "sweep value must be finite and >= 2^-1021");
         pl.P = sweep->n_points;
     }
     pl.R = n_replicas;
@@ -613,8 +650,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
 
     // workspace
     size_t off = 0;
-    pl.off_rates = off;
-    off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
+    pl.off_rates = off;  // rates [P][M] then rates_h [P][M]
+    off = align256(off + 2 * sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
     pl.off_parts = off;
     off = align256(off + (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts);
     pl.off_trace = off;
@@ -631,15 +668,22 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     return CWC_OK;
 }
 
-// per-point flat rates [P][M] (host expansion of the sweep)
+// per-point flat rates [P][M] (host expansion of the sweep),
+// followed by the same with A + A entries halved ([P][M], exact: the segment
+// kernel forms k/2 RN(x (x - 1)) == k RN(x (x - 1) / 2))
 std::vector<double> expand_rates(const cwc_model_s *m, const Plan &pl, const cwc_sweep *sweep) {
     const int M = m->M;
-    std::vector<double> rates((size_t)pl.P * std::max(M, 1), 0.0);
+    const size_t PM = (size_t)pl.P * std::max(M, 1);
+    std::vector<double> rates(2 * PM, 0.0);
     std::vector<double> rule_rates(m->rule_rate);
     for (int p = 0; p < pl.P; ++p) {
         if (sweep)
             for (int i = 0; i < sweep->n_swept; ++i) rule_rates[sweep->rule[i]] = sweep->value[(size_t)p * sweep->n_swept + i];
-        for (int k = 0; k < M; ++k) rates[(size_t)p * M + k] = rule_rates[m->entry_rule[k]];
+        for (int k = 0; k < M; ++k) {
+            const double r = rule_rates[m->entry_rule[k]];
+            rates[(size_t)p * M + k] = r;
+            rates[PM + (size_t)p * M + k] = (m->rx[k].kind >> 1) ? r * 0.5 : r;
+        }
     }
     return rates;
 }
@@ -735,6 +779,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.dt = dt;
     rp.seed = seed;
     rp.rates = (const double *)(w + pl.off_rates);
+    rp.rates_h = rp.rates + (size_t)pl.P * std::max(m->M, 1);
     rp.n_launch = pl.G;
     rp.j_stop = (int64_t)pl.J + 1;
     rp.parts = w + pl.off_parts;
@@ -837,7 +882,7 @@ constexpr size_t kHdrLive = 0, kHdrCounter = 16, kHdrOut = 32, kHdrPending = 40,
 // checked by every later call on the state: layout version, the plan's
 // shape, the shard, a hash of the flat model tables and of the per-point
 // rates, and the seed (recorded by the first advance, checked by the next).
-constexpr uint64_t kPrintMagic = 0x43574352554e0002ull;  // "CWCRUN" + layout version 2
+constexpr uint64_t kPrintMagic = 0x43574352554e0003ull;  // "CWCRUN" + layout version 3
 struct RunPrint {
     uint64_t magic;
     int64_t G, J, n_cells, M, P, O, R_total, r_off;
@@ -862,8 +907,8 @@ StateLayout state_layout(const cwc_model_s *m, const Plan &pl) {
     size_t off = 0;
     l.hdr = off;
     off = align256(off + kHdrBytes);
-    l.rates = off;
-    off = align256(off + sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
+    l.rates = off;  // rates [P][M] then rates_h [P][M]
+    off = align256(off + 2 * sizeof(double) * (size_t)pl.P * std::max(m->M, 1));
     l.parts = off;
     off = align256(off + (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts);
     l.x = off;
@@ -955,6 +1000,7 @@ RunParams run_params(const cwc_model_s *m, const Plan &pl, const StateLayout &sl
     rp.dt = dt;
     rp.seed = seed;
     rp.rates = (const double *)(st + sl.rates);
+    rp.rates_h = rp.rates + (size_t)pl.P * std::max(m->M, 1);
     rp.parts = st + sl.parts;
     rp.st = pl.st;
     rp.cells_per_part = pl.cells_per_part;

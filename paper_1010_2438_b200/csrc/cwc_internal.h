@@ -99,6 +99,7 @@ struct RunParams {
     double dt;
     uint64_t seed;
     const double *rates;    // [P][M] flat per-reaction rate constants
+    const double *rates_h;  // [P][M] the same with A + A entries halved (k / 2: segment kernel)
     // statistics: accumulator parts (see stats.cu)
     void *parts;            // n_parts x stat_bytes(st, cells_per_part)
     StatLayout st;          // word / limb layout of the parts (shared- or global-memory form)
@@ -185,6 +186,15 @@ struct WarpTables {
     const int32_t *obs_ptr;       // [O+1]
     const int32_t *obs_cells;
     const int32_t *init;          // [n_cells]
+    // per-mu header (nu offset, nu count, dependency offset, dependency
+    // count: one 16-byte load); net change entries (x byte offset, delta);
+    // dependency entries for the 16- and 32-lane chunk layouts (a slot byte
+    // offset, x_a byte offset, x_b byte offset, m * 8 | owner lane << 26 |
+    // sub << 31), read with the A + A-halved rates (RunParams.rates_h)
+    const int4 *hdr;
+    const int2 *nuw;
+    const int4 *depw16;
+    const int4 *depw32;
 };
 
 // Launchers (ssa_thread.cu, ssa_warp.cu, stats.cu); return cudaError_t.
@@ -200,6 +210,7 @@ size_t warp_smem_per_warp(const WarpTables &wt);
 cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                              size_t smem_bytes, cudaStream_t stream);
 size_t warp2_smem_per_warp(const WarpTables &wt);
+
 
 cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,
                                 cudaStream_t stream);

@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         const long long g = RES ? launch_traj(rp, (long long)gg) : (long long)gg;
         const long long p = g / rp.R;
         const double *rates = rp.rates + p * M;
+        const double *rates_h = rp.rates_h + p * M;
         const uint64_t gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);  // RNG stream id
 
         int tslot = -1;
@@ -307,29 +308,34 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             trace_rec(n, a0, tau, tn, mu);
 
             // Update: one lane per changed cell; distinct cells.
-            const int nb = __ldg(wt.nu_ptr + mu), ne = __ldg(wt.nu_ptr + mu + 1);
+            // The per-mu header (nu offset, nu count, dependency offset,
+            // dependency count) is one load.
+            const int4 h = __ldg(wt.hdr + mu);
             int2 e = make_int2(0, 0);
             long long nv = 0;
-            if (lane < ne - nb) {
-                e = __ldg(wt.nu + nb + lane);
-                nv = (long long)xs[e.x] + e.y;
+            if (lane < h.y) {
+                e = __ldg(wt.nuw + h.x + lane);  // (x byte offset, delta)
+                nv = (long long)*(const int *)((const unsigned char *)xs + e.x) + e.y;
             }
             if (__any_sync(kFull, nv > 0x7fffffffll)) {  // a count would leave int32: freeze
                 for (; j < jend; ++j) record(j);
                 status = CWC_TRAJ_OVERFLOW;
                 break;
             }
-            if (lane < ne - nb) xs[e.x] = (int)nv;
+            if (lane < h.y) *(int *)((unsigned char *)xs + e.x) = (int)nv;
             __syncwarp();
 
-            // Dependency-graph update: recompute a_m for m in D(mu) only.
+            // Dependency-graph update: recompute a_m for m in D(mu) only
+            // (byte-offset entries and A + A-halved rates: see ssa_warp2.cu).
             unsigned dirty = 0;
-            const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
-            for (int q = db + lane; q < de; q += 32) {  // (reactants inline: no dependent load of rx[m])
-                const int4 d = __ldg(wt.dep4 + q);
-                as[d.y & 0xffffff] =
-                    __dmul_rn(__ldg(rates + d.x), combos(xs[d.z], xs[d.w & 0xffffff], (d.w >> 24) & 1, d.w >> 25));
-                dirty |= 1u << (d.y >> 24);
+#pragma unroll 1
+            for (int q = lane; q < h.w; q += 32) {
+                const int4 d = __ldg(wt.depw32 + h.z + q);
+                const int xa = *(const int *)((const unsigned char *)xs + d.y);
+                const int xb = *(const int *)((const unsigned char *)xs + d.z) - (int)((unsigned)d.w >> 31);
+                const double k = __ldg((const double *)((const unsigned char *)rates_h + (d.w & 0x3ffffff)));
+                *(double *)((unsigned char *)as + d.x) = __dmul_rn(k, __dmul_rn(__int2double_rn(xa), __int2double_rn(xb)));
+                dirty |= 1u << (((unsigned)d.w >> 26) & 31u);
             }
             dirty = __reduce_or_sync(kFull, dirty);
             __syncwarp();

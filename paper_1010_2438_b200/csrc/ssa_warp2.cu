@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
     bool active = false, exhausted = false;
     long long g = 0;
     const double *rates = rp.rates;
+    const double *rates_h = rp.rates_h;
     uint64_t gk = 0;
     double t = 0.0, t_next = 0.0, a0 = 0.0, incl = 0.0, excl = 0.0, part = 0.0;
     // (kept lean: the kernel runs at 64 registers, and every live 64-bit
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
                 g = launch_traj(rp, (long long)gg);
                 const long long p = g / rp.R;
                 rates = rp.rates + p * M;
+                rates_h = rp.rates_h + p * M;
                 gk = (uint64_t)global_traj(g, rp.R, rp.R_total, rp.r_off);
                 if (TRACE) {
                     tslot = -1;
@@ -278,13 +280,14 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
         const int mu = L * B + (hit ? __ffs(hit) - 1 : (pos ? 31 - __clz(pos) : 0));
         if (TRACE && fire) trace_rec(n, a0, tau, tn, mu);
 
-        // update: one lane per changed cell
-        const int nb = fire ? __ldg(wt.nu_ptr + mu) : 0, ne = fire ? __ldg(wt.nu_ptr + mu + 1) : 0;
+        // update: one lane per changed cell; the per-mu header
+        // (nu offset, nu count, dependency offset, dependency count) is one load
+        const int4 h = fire ? __ldg(wt.hdr + mu) : make_int4(0, 0, 0, 0);
         int2 e = make_int2(0, 0);
         long long nv = 0;
-        if (sl < ne - nb) {
-            e = __ldg(wt.nu + nb + sl);
-            nv = (long long)xs[e.x] + e.y;
+        if (sl < h.y) {
+            e = __ldg(wt.nuw + h.x + sl);  // (x byte offset, delta)
+            nv = (long long)*(const int *)((const unsigned char *)xs + e.x) + e.y;
         }
         const bool ovf = ((__ballot_sync(kAll, nv > 0x7fffffffll) >> sb) & 0xffffu) != 0u;
         if (__any_sync(kAll, ovf)) {
@@ -295,21 +298,26 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp2_kernel(const RunParams rp
             }
             __syncwarp();
         }
-        if (fire && sl < ne - nb) xs[e.x] = (int)nv;
+        if (fire && sl < h.y) *(int *)((unsigned char *)xs + e.x) = (int)nv;
         __syncwarp();
 
-        // dependency-graph update: recompute a_m for m in D(mu) only
+        // dependency-graph update: recompute a_m for m in D(mu) only.  Entries
+        // carry byte offsets (slot, x_a, x_b, rate) and the owner lane; a_m =
+        // k' RN(x_a (x_b - sub)) with k' = k / 2 for A + A (rates_h): equal
+        // to k RN(binomial) bit for bit (power-of-two scaling commutes with RN)
         unsigned dirty = 0;
         if (fire) {
-            const int db = __ldg(wt.dep_ptr + mu), de = __ldg(wt.dep_ptr + mu + 1);
-            for (int q = db + sl; q < de; q += 16) {  // (reactants inline: no dependent load of rx[m])
-                const int4 d = __ldg(wt.dep16_4 + q);
-                as[d.y & 0xffffff] =
-                    __dmul_rn(__ldg(rates + d.x), combos(xs[d.z], xs[d.w & 0xffffff], (d.w >> 24) & 1, d.w >> 25));
-                dirty |= 1u << (sb + (d.y >> 24));
+#pragma unroll 1
+            for (int q = sl; q < h.w; q += 16) {
+                const int4 d = __ldg(wt.depw16 + h.z + q);
+                const int xa = *(const int *)((const unsigned char *)xs + d.y);
+                const int xb = *(const int *)((const unsigned char *)xs + d.z) - (int)((unsigned)d.w >> 31);
+                const double k = __ldg((const double *)((const unsigned char *)rates_h + (d.w & 0x3ffffff)));
+                *(double *)((unsigned char *)as + d.x) = __dmul_rn(k, __dmul_rn(__int2double_rn(xa), __int2double_rn(xb)));
+                dirty |= 1u << (((unsigned)d.w >> 26) & 31u);
             }
         }
-        dirty = __reduce_or_sync(kAll, dirty);
+        dirty = __reduce_or_sync(kAll, dirty << sb);
         __syncwarp();
         if ((dirty >> lane) & 1u) part = chunk_sum16<16>(as + sl * Bp, B);
         incl = seg_scan(part, sl, 16);
