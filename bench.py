@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 import workloads as wl  # noqa: E402
 
 METRIC = "SSA firings/sec on 1 B200 (replicas×firings); % of issue roofline"
+STATS_MODES = {"auto": 0, "shared": 1, "global": 2}
 
 # Algorithmic thread-level operations of one direct-method firing
 # (SURVEY §8(d) "Algorithmic work per firing").
@@ -310,16 +311,14 @@ def run_ours(args):
     avg_nu = float(np.mean(np.diff(flat["nu_ptr"]))) if M else 0.0
     avg_dep = float(np.mean(np.diff(flat["dep_ptr"]))) if M else 0.0
     path = "warp" if info.path == cwc.CWC_PATH_WARP else "thread"
-    # the kernel the library's automatic choice launches (cwc_api.cpp plan_run):
-    # thread path -> warp-specialised kernel; warp path -> two trajectories per
-    # warp while ceil(M/16) <= 16
-    G_all = (len(sweep["values"]) if sweep else 1) * cfg["n_replicas"]
-    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    kernel_name = (("ssa_thread_ws_kernel" if (G_all + 31) // 32 <= 8 * n_sm else "ssa_thread_kernel")
-                   if path == "thread"
-                   else ("ssa_warp2_kernel" if (M + 15) // 16 <= 16 else "ssa_warp_kernel"))
-
     R = cfg["n_replicas"]
+    plan_opts = cwc.cwc_sim_opts()
+    plan_opts.force_path = cwc.CWC_PATH_AUTO
+    plan_opts.stats_mode = STATS_MODES[args.stats_mode]
+    plan_opts.replica_offset = rank * R
+    plan_opts.replicas_total = world * R
+    plan = cwc.cwc_plan(model, R, sweep, cfg["t_end"], cfg["sample_dt"], plan_opts)
+    kernel_name = cwc.KERNEL_NAMES[plan.kernel]  # the kernel the library's plan launches
     P = len(sweep["values"]) if sweep else 1
     J1 = int(np.floor(cfg["t_end"] / cfg["sample_dt"])) + 1
     O = info.n_obs
@@ -332,10 +331,18 @@ def run_ours(args):
     firings = torch.empty(G, dtype=torch.int64, device=dev)
     status = torch.empty(G, dtype=torch.int32, device=dev)
     ev_k0, ev_k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev_k0.record(stream)
-    ev_k1.record(stream)
+    ev_s0, ev_s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for ev in (ev_k0, ev_k1, ev_s0, ev_s1):
+        ev.record(stream)
     opts = cwc.cwc_sim_opts()
     opts.force_path = cwc.CWC_PATH_AUTO
+    opts.stats_mode = STATS_MODES[args.stats_mode]
+    opts.ev_stage2_begin = ev_s0.cuda_event
+    opts.ev_stage2_end = ev_s1.cuda_event
+    traj = None
+    if args.dump:  # trajectory dump mode: every sampled observable written to HBM (int64 [G][J+1][O])
+        traj = torch.empty((G, J1, O), dtype=torch.int64, device=dev)
+        opts.out_traj = traj.data_ptr()
     opts.out_firings = firings.data_ptr()
     opts.out_status = status.data_ptr()
     opts.replica_offset = rank * R
@@ -358,7 +365,7 @@ def run_ours(args):
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kms = []
+    kms, sms = [], []
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     clocks = ClockSampler(vis.split(",")[local] if vis else local)
     if world > 1:
@@ -372,6 +379,7 @@ def run_ours(args):
         ev1[k].record(stream)
         ev1[k].synchronize()
         kms.append(ev_k0.elapsed_time(ev_k1))
+        sms.append(ev_s0.elapsed_time(ev_s1))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -426,15 +434,32 @@ def run_ours(args):
                 "peak_source": "issue peak = %d SMs x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
                 % (props.multi_processor_count, f_max / 1e6)}
 
+    # stage 2 (HBM-bound): algorithmic bytes = every accumulator part read
+    # once + the output cells written once (count, sum: 8 B; sumsq: 16 B)
+    s_ms = float(np.mean(sms))
+    s_bytes = plan.n_parts * plan.part_cells * plan.word_bytes * plan.words_per_cell + 32 * ncell
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    stage2 = {"kernel": "stats_stage2_kernel", "ms": s_ms, "algorithmic_bytes": s_bytes,
+              "gbs": s_bytes / (s_ms * 1e-3) / 1e9 if s_ms > 0 else None, "peak_gbs": hbm,
+              "frac": (s_bytes / (s_ms * 1e-3) / 1e9) / hbm if s_ms > 0 else None,
+              "parts": plan.n_parts, "shared_memory_parts": bool(plan.stats_shared)}
     line = {"metric": METRIC, "value": value, "unit": "firings/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_block(args.config, cfg, sweep, world, path),
+            "config": dict(_config_block(args.config, cfg, sweep, world, path), kernel=kernel_name,
+                           stats=("shared-memory parts" if plan.stats_shared else "one global part") +
+                           " (--stats-mode %s)" % args.stats_mode, dump=bool(args.dump)),
             "firings_per_step": fired_all, "kernel_ms_per_step": k_ms,
             "roofline": roofline,
-            "e2e": {"value": e2e_value, "unit": "firings/s", "h2d_bytes_per_step": 8 * P * max(M, 1),
+            "e2e": {"value": e2e_value, "unit": "firings/s", "h2d_bytes_per_step": 16 * P * max(M, 1) +
+                    (4 * plan.blocks if (path == "thread" and P > 1) else 0),
                     "d2h_bytes_per_step": 32 * ncell},
+            "stage2": stage2,
             "gpu_launches": 2 * args.steps, "clocks": clk}
+    if args.dump:
+        dump_bytes = G * J1 * O * 8
+        line["dump"] = {"bytes_per_step": dump_bytes, "kernel_ms": k_ms,
+                        "gbs": dump_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": hbm}
     if comm_ok is not None:
         line["comm"] = {"backend": "nccl", "world_size": world, "comm_nranks_ok": comm_ok,
                         "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
@@ -463,6 +488,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stats-mode", default="auto", choices=sorted(STATS_MODES))
+    ap.add_argument("--dump", action="store_true", help="also write every trajectory sample to HBM (dump mode)")
     ap.add_argument("--no-all-cores", action="store_true", help="skip the all-host-cores oracle line")
     ap.add_argument("--selftest-dist", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()

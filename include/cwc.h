@@ -180,6 +180,10 @@ typedef struct {
     int32_t stats_mode;
     int32_t warps_per_block;
     int32_t blocks_per_sm;
+    /* optional cudaEvent_t pair recorded on cuda_stream right before and
+       after the stage-2 reduction of the moments (its HBM bandwidth) */
+    void *ev_stage2_begin;
+    void *ev_stage2_end;
 } cwc_sim_opts;
 
 /* Summary of a created model (cwc_model_info). */
@@ -220,6 +224,25 @@ cwc_status cwc_model_get_flat(cwc_model model, int32_t *entry_rule, int32_t *ent
                               int32_t *entry_child, int32_t *re_ptr, int32_t *re_cell, int32_t *re_mult,
                               int32_t *nu_ptr, int32_t *nu_cell, int32_t *nu_delta,
                               int32_t *dep_ptr, int32_t *dep);
+
+/* The launch plan cwc_simulate would use for these arguments (host only,
+ * no device work): which kernel, its grid, and the statistics accumulators
+ * (for measurement: bench.py's roofline and stage-2 bandwidth). */
+typedef struct {
+    int32_t kernel;          /* CWC_KERNEL_* actually launched (never AUTO) */
+    int32_t blocks;          /* CTAs of the SSA kernel */
+    int32_t threads;         /* threads per CTA */
+    int32_t stats_shared;    /* 1: per-CTA shared-memory parts, 0: one global part */
+    int64_t smem_bytes;      /* dynamic shared memory per CTA */
+    int64_t n_parts;         /* statistics parts stage 2 reduces */
+    int64_t part_cells;      /* cells per part */
+    int32_t word_bytes;      /* bytes per accumulator word (4 shared, 8 global) */
+    int32_t words_per_cell;  /* count word + sum limbs + sum-of-squares limbs */
+    int64_t n_stat_cells;    /* output cells: points * (J+1) * n_obs */
+    int64_t workspace_bytes; /* = cwc_simulate_workspace_size */
+} cwc_plan_info;
+cwc_status cwc_plan(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                    const cwc_sim_opts *opts, cwc_plan_info *info);
 
 /* Workspace (device bytes) cwc_simulate needs for these arguments. */
 cwc_status cwc_simulate_workspace_size(cwc_model model, int64_t n_replicas, const cwc_sweep *sweep,

@@ -40,6 +40,17 @@ cwc_status cuda_fail(cudaError_t e, const char *where) {
     return CWC_ERR_CUDA;
 }
 
+// FNV-1a over bytes (input fingerprints: staging cache, resumable-state header)
+uint64_t fnv1a(uint64_t h, const void *p, size_t n) {
+    const unsigned char *b = (const unsigned char *)p;
+    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+    return h;
+}
+template <typename T>
+uint64_t fnv_vec(uint64_t h, const std::vector<T> &v) {
+    return fnv1a(h, v.data(), v.size() * sizeof(T));
+}
+
 struct DeviceBuf {
     void *p = nullptr;
     ~DeviceBuf() {
@@ -79,6 +90,23 @@ struct cwc_model_s {
     };
     std::mutex dev_mu;
     std::map<int, std::unique_ptr<DevCopy>> dev;
+    // Pinned host staging of a call's per-point rates and sweep dispatch
+    // order, per device: cudaMemcpyAsync from pinned memory does not stall
+    // the host, and consecutive calls with the same inputs (a bench loop, a
+    // checkpointed run) reuse the staged bytes without recomputing them.
+    struct Stage {
+        uint64_t key = 0;
+        bool valid = false;
+        unsigned char *pinned = nullptr;
+        size_t cap = 0, rates_bytes = 0, order_off = 0, order_bytes = 0;
+        cudaEvent_t done = nullptr;  // the last copies out of `pinned` have finished
+        ~Stage() {
+            if (done) cudaEventDestroy(done);
+            if (pinned) cudaFreeHost(pinned);
+        }
+    };
+    std::mutex stage_mu;
+    std::map<int, Stage> stage;
 };
 
 namespace {
@@ -765,9 +793,61 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     cudaStream_t stream = (cudaStream_t)stream_;
     unsigned char *w = (unsigned char *)ws;
 
-    const std::vector<double> rates = expand_rates(m, pl, sweep);
-    cudaError_t e = cudaMemcpyAsync(w + pl.off_rates, rates.data(), sizeof(double) * rates.size(), cudaMemcpyHostToDevice, stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: rates upload");
+    // per-point rates (and, for sweeps on the thread path, the dispatch
+    // order) through the model's pinned staging (cwc_model_s::Stage)
+    const bool want_order = pl.path == CWC_PATH_THREAD && pl.P > 1;
+    const int T_order = pl.ws ? 32 * kWsGroups : pl.threads;
+    cudaError_t e = cudaSuccess;
+    {
+        uint64_t key = 0xcbf29ce484222325ull;
+        const int64_t shape[6] = {pl.P, m->M, pl.R, pl.blocks, want_order ? T_order : 0, sweep ? sweep->n_swept : -1};
+        key = fnv1a(key, shape, sizeof(shape));
+        if (sweep && sweep->n_swept > 0) {
+            key = fnv1a(key, sweep->rule, sizeof(int32_t) * sweep->n_swept);
+            key = fnv1a(key, sweep->value, sizeof(double) * (size_t)sweep->n_points * sweep->n_swept);
+        }
+        int device = 0;
+        if ((e = cudaGetDevice(&device)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: cudaGetDevice");
+        std::lock_guard<std::mutex> lock(m->stage_mu);
+        cwc_model_s::Stage &sg = m->stage[device];
+        if (!sg.valid || sg.key != key) {
+            if (sg.done && (e = cudaEventSynchronize(sg.done)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: staging");
+            const std::vector<double> rates = expand_rates(m, pl, sweep);
+            std::vector<int32_t> order;
+            // Parameter sweeps: trajectory lengths differ by point (C3: 17x),
+            // and CTAs start in blockIdx order as the SMs free up.  Dispatch
+            // the groups longest-expected-first (LPT), estimating a group's
+            // work by the total propensity a0(x0) of its trajectories' points
+            // (firings per unit time at t = 0).  Trajectory ids -- hence the
+            // RNG streams and every result -- are unchanged; only the start
+            // order moves.
+            if (want_order) order = lpt_groups(pl, point_a0(m, pl, rates), T_order);
+            sg.rates_bytes = sizeof(double) * rates.size();
+            sg.order_off = align256(sg.rates_bytes);
+            sg.order_bytes = sizeof(int32_t) * order.size();
+            const size_t need = sg.order_off + sg.order_bytes;
+            if (need > sg.cap) {
+                if (sg.pinned) cudaFreeHost(sg.pinned);
+                sg.pinned = nullptr;
+                sg.cap = 0;
+                sg.valid = false;
+                if ((e = cudaHostAlloc((void **)&sg.pinned, need, cudaHostAllocDefault)) != cudaSuccess)
+                    return cuda_fail(e, "cwc_simulate: pinned staging");
+                sg.cap = need;
+            }
+            std::memcpy(sg.pinned, rates.data(), sg.rates_bytes);
+            if (!order.empty()) std::memcpy(sg.pinned + sg.order_off, order.data(), sg.order_bytes);
+            if (!sg.done && (e = cudaEventCreateWithFlags(&sg.done, cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(e, "cwc_simulate: staging event");
+            sg.key = key;
+            sg.valid = true;
+        }
+        e = cudaMemcpyAsync(w + pl.off_rates, sg.pinned, sg.rates_bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess && want_order)
+            e = cudaMemcpyAsync(w + pl.off_order, sg.pinned + sg.order_off, sg.order_bytes, cudaMemcpyHostToDevice, stream);
+        if (e == cudaSuccess) e = cudaEventRecord(sg.done, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: rates upload");
+    }
 
     RunParams rp{};
     rp.G = pl.G;
@@ -812,20 +892,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         e = cudaMemsetAsync(w + pl.off_parts, 0, (size_t)stat_bytes(pl.st, pl.cells_per_part) * pl.n_parts, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: zero partials");
     }
-    if (pl.path == CWC_PATH_THREAD && pl.P > 1) {
-        // Parameter sweeps: trajectory lengths differ by point (C3: 17x), and
-        // CTAs start in blockIdx order as the SMs free up.  Dispatch the
-        // groups longest-expected-first (LPT), estimating a group's work by
-        // the total propensity a0(x0) of its trajectories' points (firings per
-        // unit time at t = 0).  Trajectory ids -- hence the RNG streams and
-        // every result -- are unchanged; only the start order moves.
-        const int T = pl.ws ? 32 * kWsGroups : pl.threads;
-        // pageable source: cudaMemcpyAsync has copied it when it returns
-        const std::vector<int32_t> order_host = lpt_groups(pl, point_a0(m, pl, rates), T);
-        e = cudaMemcpyAsync(w + pl.off_order, order_host.data(), sizeof(int32_t) * pl.blocks, cudaMemcpyHostToDevice, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: dispatch order upload");
-        rp.cta_order = (const int32_t *)(w + pl.off_order);
-    }
+    if (want_order) rp.cta_order = (const int32_t *)(w + pl.off_order);
     // Alternating consumer/producer placement per SM (CWC_WS_MIX=1) was
     // measured slower on C2: a producer's fp64-heavy log stream on the same
     // sub-partition delays the consumer's fp64 chain more than a second
@@ -854,8 +921,12 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
         dst.sumsq = (uint64_t *)(sb + 16 * pl.n_stat_cells);
     }
     if (pl.n_stat_cells > 0) {
+        cudaEvent_t es0 = opts ? (cudaEvent_t)opts->ev_stage2_begin : nullptr;
+        cudaEvent_t es1 = opts ? (cudaEvent_t)opts->ev_stage2_end : nullptr;
+        if (es0 && (e = cudaEventRecord(es0, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_stage2_begin");
         e = launch_stats_stage2(rp, m->n_obs, dst.count, dst.sum, dst.sumsq, stream);
         if (e != cudaSuccess) return cuda_fail(e, "cwc_simulate: stage-2 launch");
+        if (es1 && (e = cudaEventRecord(es1, stream)) != cudaSuccess) return cuda_fail(e, "cwc_simulate: ev_stage2_end");
         if (host_stats) {
             const size_t n8 = 8 * (size_t)pl.n_stat_cells;
             if ((e = cudaMemcpyAsync(host_out.count, dst.count, n8, cudaMemcpyDeviceToHost, stream)) != cudaSuccess ||
@@ -891,15 +962,6 @@ struct RunPrint {
 };
 static_assert(kHdrPrint + sizeof(RunPrint) <= kHdrBytes, "header too small");
 
-uint64_t fnv1a(uint64_t h, const void *p, size_t n) {
-    const unsigned char *b = (const unsigned char *)p;
-    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
-    return h;
-}
-template <typename T>
-uint64_t fnv_vec(uint64_t h, const std::vector<T> &v) {
-    return fnv1a(h, v.data(), v.size() * sizeof(T));
-}
 
 StateLayout state_layout(const cwc_model_s *m, const Plan &pl) {
     StateLayout l;
@@ -1230,6 +1292,28 @@ cwc_status cwc_model_get_flat(cwc_model m, int32_t *entry_rule, int32_t *entry_c
     cp(nu_delta, m->nu_delta);
     cp(dep_ptr, m->dep_ptr);
     cp(dep, m->dep);
+    return CWC_OK;
+}
+
+cwc_status cwc_plan(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t_end, double sample_dt,
+                    const cwc_sim_opts *opts, cwc_plan_info *info) {
+    if (!info) return fail(CWC_ERR_INVALID, "info is NULL");
+    Plan pl;
+    cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl);
+    if (s != CWC_OK) return s;
+    info->kernel = pl.path == CWC_PATH_THREAD ? (pl.ws ? CWC_KERNEL_THREAD_WS : CWC_KERNEL_THREAD)
+                                              : (pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
+    info->blocks = pl.path == CWC_PATH_THREAD ? (pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)
+                                              : pl.blocks;
+    info->threads = pl.path == CWC_PATH_THREAD ? (pl.ws ? 32 * (1 + kWsProducers) * kWsGroups : pl.threads) : pl.threads;
+    info->stats_shared = pl.stats_smem;
+    info->smem_bytes = (int64_t)pl.smem_bytes;
+    info->n_parts = pl.n_parts;
+    info->part_cells = pl.cells_per_part;
+    info->word_bytes = pl.st.wb;
+    info->words_per_cell = stat_words(pl.st);
+    info->n_stat_cells = pl.n_stat_cells;
+    info->workspace_bytes = (int64_t)pl.total;
     return CWC_OK;
 }
 

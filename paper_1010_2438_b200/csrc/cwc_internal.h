@@ -46,7 +46,13 @@ __host__ __device__ __forceinline__ long long stat_bytes(const StatLayout &l, lo
 }
 // warp-specialised thread path (ssa_thread_ws.cuh): draws in flight per
 // trajectory and the ring + hand-off counters' shared-memory bytes per CTA
-constexpr int kWsRing = 32;
+// CWC_WS_STRESS (test builds only, tests/test_gpu_ws_stress.py): the
+// smallest legal ring and pseudo-random sleeps in producer and consumer, so
+// the hand-off runs in every interleaving order the timing can produce
+#ifndef CWC_WS_STRESS
+#define CWC_WS_STRESS 0
+#endif
+constexpr int kWsRing = CWC_WS_STRESS ? 8 : 32;
 #ifndef CWC_WS_PRODUCERS
 #define CWC_WS_PRODUCERS 1
 #endif

@@ -45,6 +45,20 @@ namespace cwc {
 // never overwrite a slot the consumer has not read yet), acquire load by
 // the producer.  done: relaxed (it orders nothing: the producer only stops).
 __device__ __forceinline__ unsigned smem_addr(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+// Stress builds: a pseudo-random sleep of 0 .. ~4 us on a quarter of the
+// calls (hash of the trajectory, the counter and a salt), different per lane.
+__device__ __forceinline__ void ws_stress_sleep(unsigned long long g, unsigned long long k, unsigned salt) {
+#if CWC_WS_STRESS
+    unsigned long long h = (g * 0x9E3779B97F4A7C15ull) ^ (k * 0xC2B2AE3D27D4EB4Full) ^ ((unsigned long long)salt << 17);
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    if ((h & 3u) == 0u) __nanosleep((unsigned)(h >> 40) & 4095u);
+#else
+    (void)g; (void)k; (void)salt;
+#endif
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
@@ -164,6 +178,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
                         ringE[slot * 32 + lane] = Ew[i];
                         ringU[slot * 32 + lane] = Uw[i];
                     }
+                    ws_stress_sleep(gk, rounds, 1u);  // (stress builds: between the slot writes and the release)
                     ++rounds;
                     st_release(prod + q * 32 + lane, rounds);
                 }
@@ -382,6 +397,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
                 if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
             }
             if (prof) { c1 = clock64(); pc[3] += c1 - c0; c0 = c1; }
+            ws_stress_sleep(gk, n, 2u);  // (stress builds: between the slot reads and the release)
             // release consumed slots (the slot reads above are ordered before it)
             st_release(cons + lane, (unsigned)n);
             if (in_range && !live) st_relaxed(done + lane, 1u);

@@ -24,7 +24,7 @@ CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
 CWC_KERNEL_AUTO, CWC_KERNEL_THREAD_WS, CWC_KERNEL_THREAD, CWC_KERNEL_WARP2, CWC_KERNEL_WARP = 0, 1, 2, 3, 4
 CWC_STATS_AUTO, CWC_STATS_SHARED, CWC_STATS_GLOBAL = 0, 1, 2
 
-EXPORTED = ["cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
+EXPORTED = ["cwc_plan", "cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
             "cwc_simulate_workspace_size", "cwc_simulate", "cwc_simulate_host", "cwc_simulate_host_workspace_size",
             "cwc_stats_finalize", "cwc_philox_blocks", "cwc_draws", "cwc_block_draws", "cwc_tau_div", "cwc_run_state_size",
             "cwc_run_init", "cwc_run_advance", "cwc_run_stats", "cwc_last_error"]
@@ -60,7 +60,14 @@ class cwc_sim_opts(ctypes.Structure):
     _fields_ = [("out_traj", P), ("out_firings", P), ("out_status", P), ("trace_g", P), ("n_trace", I32),
                 ("trace_cap", I64), ("trace_buf", P), ("trace_len", P), ("force_path", I32), ("block_threads", I32),
                 ("replica_offset", I64), ("replicas_total", I64), ("ev_kernel_begin", P), ("ev_kernel_end", P),
-                ("kernel", I32), ("stats_mode", I32), ("warps_per_block", I32), ("blocks_per_sm", I32)]
+                ("kernel", I32), ("stats_mode", I32), ("warps_per_block", I32), ("blocks_per_sm", I32),
+                ("ev_stage2_begin", P), ("ev_stage2_end", P)]
+
+
+class cwc_plan_info(ctypes.Structure):
+    _fields_ = [("kernel", I32), ("blocks", I32), ("threads", I32), ("stats_shared", I32), ("smem_bytes", I64),
+                ("n_parts", I64), ("part_cells", I64), ("word_bytes", I32), ("words_per_cell", I32),
+                ("n_stat_cells", I64), ("workspace_bytes", I64)]
 
 
 class cwc_model_info(ctypes.Structure):
@@ -83,6 +90,7 @@ def lib():
         L.cwc_model_destroy.restype = None
         L.cwc_model_info_get.argtypes = [P, ctypes.POINTER(cwc_model_info)]
         L.cwc_model_get_flat.argtypes = [P] + [P] * 11
+        L.cwc_plan.argtypes = [P, I64, P, ctypes.c_double, ctypes.c_double, P, ctypes.POINTER(cwc_plan_info)]
         L.cwc_simulate_workspace_size.argtypes = [P, I64, P, ctypes.c_double, ctypes.c_double, P, ctypes.POINTER(ctypes.c_size_t)]
         L.cwc_simulate.argtypes = [P, I64, P, ctypes.c_double, ctypes.c_double, ctypes.c_uint64, P, cwc_stats, P,
                                    ctypes.c_size_t, P]
@@ -224,6 +232,19 @@ def cwc_simulate_workspace_size(model, n_replicas, sweep, t_end, sample_dt, opts
                                              float(t_end), float(sample_dt), ctypes.byref(opts) if opts else None,
                                              ctypes.byref(n)))
     return n.value
+
+
+KERNEL_NAMES = {CWC_KERNEL_THREAD_WS: "ssa_thread_ws_kernel", CWC_KERNEL_THREAD: "ssa_thread_kernel",
+                CWC_KERNEL_WARP2: "ssa_warp2_kernel", CWC_KERNEL_WARP: "ssa_warp_kernel"}
+
+
+def cwc_plan(model, n_replicas, sweep, t_end, sample_dt, opts=None):
+    """The launch plan (cwc_plan_info) cwc_simulate would use."""
+    sw = _SweepArrays(sweep) if sweep is not None else None
+    info = cwc_plan_info()
+    _check(lib().cwc_plan(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
+                          float(sample_dt), ctypes.byref(opts) if opts else None, ctypes.byref(info)))
+    return info
 
 
 def cwc_simulate(model, n_replicas, sweep, t_end, sample_dt, seed, stream, stats, workspace, opts=None):

@@ -233,3 +233,27 @@ def test_int64_moment_bound():
     with pytest.raises(cwc.CwcError) as ei:
         cwc.cwc_simulate_workspace_size(m, 16, None, 1.0, 0.1, _opts(replicas_total=2**28))
     assert ei.value.status == cwc.CWC_ERR_INVALID
+
+
+def test_plan_reports_the_kernel_and_accumulators():
+    """cwc_plan: the automatic plan per config (148 SMs assumed without a
+    GPU): the warp-specialised thread kernel while at most two CTAs share an
+    SM (C1), the single-warp thread kernel beyond (C2, C3), two trajectories
+    per warp for M <= 256 (C4), one per warp above (C5); statistics layout
+    consistent with the workspace size."""
+    want = {"C1": cwc.CWC_KERNEL_THREAD_WS, "C2": cwc.CWC_KERNEL_THREAD, "C3": cwc.CWC_KERNEL_THREAD,
+            "C4": cwc.CWC_KERNEL_WARP2, "C5": cwc.CWC_KERNEL_WARP}
+    for name, k in want.items():
+        d, sweep, cfg = w.config(name)
+        m = cwc.cwc_model_create(d)
+        p = cwc.cwc_plan(m, cfg["n_replicas"], sweep, cfg["t_end"], cfg["sample_dt"])
+        assert p.kernel == k, name
+        P = len(sweep["values"]) if sweep else 1
+        assert p.n_stat_cells == P * (int(cfg["t_end"] / cfg["sample_dt"] + 1e-9) + 1) * m.info.n_obs
+        assert p.workspace_bytes == cwc.cwc_simulate_workspace_size(m, cfg["n_replicas"], sweep, cfg["t_end"],
+                                                                   cfg["sample_dt"])
+        assert p.word_bytes in (4, 8) and p.words_per_cell >= 3 and p.n_parts >= 1
+        assert p.part_cells >= p.n_stat_cells if not p.stats_shared else p.part_cells > 0
+    m = cwc.cwc_model_create(w.config("C2")[0])
+    assert cwc.cwc_plan(m, 64, None, 1.0, 0.1, _opts(kernel=cwc.CWC_KERNEL_WARP)).kernel == cwc.CWC_KERNEL_WARP
+    assert cwc.cwc_plan(m, 64, None, 1.0, 0.1, _opts(force_path=cwc.CWC_PATH_WARP)).kernel == cwc.CWC_KERNEL_WARP2

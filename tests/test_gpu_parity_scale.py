@@ -76,6 +76,10 @@ def oracle_subset(name, g_list):
 
 @pytest.mark.parametrize("name,stride", SUBSETS, ids=[s[0] for s in SUBSETS])
 def test_parity_at_survey_scale(name, stride):
+    run_parity(name, stride)
+
+
+def run_parity(name, stride, tag="parity"):
     desc, sweep, cfg = w.config(name)
     model = cwc.cwc_model_create(desc)
     R = cfg["n_replicas"]
@@ -98,6 +102,7 @@ def test_parity_at_survey_scale(name, stride):
     assert torch.equal(gpu["sumsq"][..., 0], (t * t).sum(dim=1))
 
     g_list = list(range(0, G, stride))
+    del t
     t0 = time.time()
     o_traj, o_fir, o_st = oracle_subset(name, g_list)
     t_oracle = time.time() - t0
@@ -123,7 +128,7 @@ def test_parity_at_survey_scale(name, stride):
     dst = os.environ.get("CWC_PARITY_OUT")
     if dst:
         os.makedirs(dst, exist_ok=True)
-        with open(os.path.join(dst, "parity_%s.json" % name), "w") as f:
+        with open(os.path.join(dst, "%s_%s.json" % (tag, name)), "w") as f:
             json.dump(out, f, indent=1)
     for rec in report:
         assert rec[1] not in ("BUG", "identical-trace"), rec
