@@ -591,9 +591,14 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // beyond the statistics part: the draw ring + staging of the
         // warp-specialised CTA, or the record staging of each warp
         const size_t extra = (ws ? kWsRingBytes : (size_t)(T / 32) * kStageLL * sizeof(long long)) + kNegLogSmemBytes;
-        const int64_t resident_needed = (blocks + nsm - 1) / nsm;
-        bool use_smem = smem + extra <= smem_cap &&
-                        (int64_t)(smem + extra) * std::min<int64_t>(resident_needed, 2048 / T) <= (int64_t)smem_cap;
+        // One global part (fire-and-forget 64-bit REDs to L2) by default:
+        // measured faster than per-CTA shared-memory parts on every config
+        // (profiles/r02/stats_modes.json: C1 4.60e9 vs 4.17e9, C2 8.95e10 vs
+        // 4.56e10, C3 6.77 vs 7.27 ms per step); crossings are too rare for
+        // L2 contention, and shared parts cost occupancy, zeroing and a
+        // larger stage 2.  CWC_STATS_SHARED keeps the block-level reduction
+        // available (same results bit for bit).
+        bool use_smem = false;
         if (smode == CWC_STATS_SHARED) {
             if (smem + extra > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
             use_smem = true;
@@ -634,10 +639,10 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t stats = (size_t)stat_bytes(lay_s, cells);
-        // shared-memory statistics only while they cost no occupancy (the
-        // kernel holds 8 CTAs of 4 warps per SM): crossings are rare, so the
-        // global-memory parts (fire-and-forget REDs to L2) are nearly free
-        bool use_smem = (stats + W * per_warp) * 8 <= 200 * 1024;
+        // one global part by default (see the thread path; C4 4.58e9 vs
+        // 0.86e9, C5 1.50e9 vs 0.46e9 with shared-memory parts, which halve
+        // the resident warps)
+        bool use_smem = false;
         if (smode == CWC_STATS_SHARED) {
             if (stats + W * per_warp > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
             use_smem = true;
