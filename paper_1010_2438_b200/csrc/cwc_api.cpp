@@ -456,6 +456,7 @@ struct Plan {
     int stats_smem = 0;
     int ws = 0;
     int seg2 = 0;  // warp path: two trajectories per warp
+    int nt = 1;    // thread path, single-warp kernel: trajectories per lane
     StatLayout st{};
     int64_t cells_per_part = 0;
     int n_parts = 1;
@@ -520,12 +521,12 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     const int smode = opts ? opts->stats_mode : CWC_STATS_AUTO;
     const int wpb = opts ? opts->warps_per_block : 0;
     const int bps = opts ? opts->blocks_per_sm : 0;
-    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_WARP) return fail(CWC_ERR_INVALID, "bad kernel");
+    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_THREAD2) return fail(CWC_ERR_INVALID, "bad kernel");
     if (smode < CWC_STATS_AUTO || smode > CWC_STATS_GLOBAL) return fail(CWC_ERR_INVALID, "bad stats_mode");
     if (wpb < 0 || wpb > 4) return fail(CWC_ERR_INVALID, "warps_per_block must be in [0, 4]");
     if (bps < 0 || bps > 32) return fail(CWC_ERR_INVALID, "blocks_per_sm must be in [0, 32]");
     if (force != CWC_PATH_AUTO && force != CWC_PATH_THREAD && force != CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "bad force_path");
-    if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD) {
+    if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD || kern == CWC_KERNEL_THREAD2) {
         if (force == CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_THREAD;
     } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP) {
@@ -568,20 +569,27 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             if (resumable) return fail(CWC_ERR_INVALID, "resumable runs do not use the warp-specialised kernel");
             if (bt && bt != 32 * kWsGroups) return fail(CWC_ERR_INVALID, "the warp-specialised kernel has a fixed CTA shape (block_threads)");
             ws = true;
-        } else if (kern == CWC_KERNEL_THREAD) {
+        } else if (kern == CWC_KERNEL_THREAD || kern == CWC_KERNEL_THREAD2) {
             ws = false;
         }
         if (resumable) ws = false;
         if (ws) T = 32 * kWsGroups;
         pl.ws = ws ? 1 : 0;
         pl.threads = T;
-        const int64_t blocks = (NL + T - 1) / T;
+        // single-warp kernel: two trajectories per lane (ssa_thread_impl.cuh
+        // NT) only on request -- measured 3x slower on C2/C3 (the doubled
+        // per-trajectory state spills at 255 registers)
+        pl.nt = (!ws && !resumable && pl.m_pad <= 8 && kern == CWC_KERNEL_THREAD2) ? 2 : 1;
+        if (kern == CWC_KERNEL_THREAD2 && pl.nt != 2)
+            return fail(CWC_ERR_INVALID, "kernel THREAD2 needs M <= 8 and a one-shot run");
+        const int64_t blocks = (NL + (int64_t)T * pl.nt - 1) / ((int64_t)T * pl.nt);
         if (blocks > 0x7fffffffll) return fail(CWC_ERR_INVALID, "too many trajectories for one launch");
         pl.blocks = (int)blocks;
         // points touched by one block
         int64_t np_max = 1;
+        const int64_t TB = (int64_t)T * pl.nt;  // trajectories per block
         for (int64_t b = 0; b < blocks; ++b) {
-            const int64_t pf = (b * T) / pl.R, plst = (std::min<int64_t>((b + 1) * T, pl.G) - 1) / pl.R;
+            const int64_t pf = (b * TB) / pl.R, plst = (std::min<int64_t>((b + 1) * TB, pl.G) - 1) / pl.R;
             np_max = std::max(np_max, plst - pf + 1);
             if (np_max >= pl.P) break;
         }
@@ -609,7 +617,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             pl.st = lay_s;
             pl.cells_per_part = std::max<int64_t>(cells, 4);
             pl.n_parts = pl.blocks;
-            pl.traj_per_part = T;
+            pl.traj_per_part = (int64_t)T * pl.nt;
             pl.smem_bytes = smem + extra;
         } else {
             pl.stats_smem = 0;
@@ -801,7 +809,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     // per-point rates (and, for sweeps on the thread path, the dispatch
     // order) through the model's pinned staging (cwc_model_s::Stage)
     const bool want_order = pl.path == CWC_PATH_THREAD && pl.P > 1;
-    const int T_order = pl.ws ? 32 * kWsGroups : pl.threads;
+    const int T_order = pl.ws ? 32 * kWsGroups : pl.threads * pl.nt;
     cudaError_t e = cudaSuccess;
     {
         uint64_t key = 0xcbf29ce484222325ull;
@@ -871,6 +879,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.cells_per_part = pl.cells_per_part;
     rp.st = pl.st;
     rp.ws = pl.ws;
+    rp.thread_nt = pl.nt;
     rp.stats_smem = pl.stats_smem;
     rp.n_parts = pl.n_parts;
     rp.traj_per_part = pl.traj_per_part;
@@ -1306,8 +1315,9 @@ cwc_status cwc_plan(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, dou
     Plan pl;
     cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl);
     if (s != CWC_OK) return s;
-    info->kernel = pl.path == CWC_PATH_THREAD ? (pl.ws ? CWC_KERNEL_THREAD_WS : CWC_KERNEL_THREAD)
-                                              : (pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
+    info->kernel = pl.path == CWC_PATH_THREAD
+                       ? (pl.ws ? CWC_KERNEL_THREAD_WS : (pl.nt == 2 ? CWC_KERNEL_THREAD2 : CWC_KERNEL_THREAD))
+                       : (pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
     info->blocks = pl.path == CWC_PATH_THREAD ? (pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)
                                               : pl.blocks;
     info->threads = pl.path == CWC_PATH_THREAD ? (pl.ws ? 32 * (1 + kWsProducers) * kWsGroups : pl.threads) : pl.threads;

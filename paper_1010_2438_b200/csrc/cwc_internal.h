@@ -112,6 +112,7 @@ struct RunParams {
     int64_t cells_per_part;
     int32_t stats_smem;     // 1: block accumulators in shared memory, flushed to parts[blockIdx]
     int32_t ws;             // thread path: warp-specialised producer/consumer kernel (ssa_thread_ws.cuh)
+    int32_t thread_nt;      // thread path, single-warp kernel: trajectories per lane (1 or 2)
     const int32_t *cta_order;  // thread path: CTA slot -> trajectory group (NULL = identity)
     unsigned *sm_ctr;          // warp-specialised kernel: per-SM CTA arrival counters (zeroed per call)
     int32_t part_stride_blocks;  // GLOBAL mode: block b accumulates into part (b % n_parts)

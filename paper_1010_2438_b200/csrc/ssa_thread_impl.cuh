@@ -332,16 +332,23 @@ struct ThreadBatch {
 };
 
 // RES: resumable runs (cwc_run_*: state load/save, launch bounds); the
-// one-shot instantiations carry none of it
-template <int S, int M, bool TRACE, bool RES>
+// one-shot instantiations carry none of it.
+// NT: trajectories per lane (1 or 2).  With NT = 2 a lane runs two
+// trajectories (consecutive ids) whose batches are interleaved in one
+// straight-line block: the two state chains are independent, so the
+// in-order issue of a lone warp sees twice the instruction-level parallelism
+// (C2 has fewer trajectory warps than the chip has sub-partitions; measured:
+// two warps per sub-partition raise its firings/s 1.4x).  Each trajectory's
+// batch is B / NT firings, so the draws in flight per lane stay B.
+template <int S, int M, bool TRACE, bool RES, int NT>
 __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
-    constexpr int B = ThreadBatch<M>::B;
+    constexpr int B = (NT == 2 && ThreadBatch<M>::B >= 2) ? ThreadBatch<M>::B / 2 : ThreadBatch<M>::B;
+    static_assert(NT == 1 || NT == 2, "one or two trajectories per lane");
     extern __shared__ __align__(16) unsigned char smem[];
     const long long T = blockDim.x;
     // dispatch order: CTA slot blockIdx.x runs trajectory group cta (RunParams.cta_order)
     const long long cta = rp.cta_order ? (long long)__ldg(rp.cta_order + blockIdx.x) : (long long)blockIdx.x;
-    const long long g0 = cta * T;  // first launch slot of the CTA
-    const long long slot = g0 + threadIdx.x;
+    const long long g0 = cta * T * NT;  // first launch slot of the CTA
     const int O = tt.O;
     const long long J = rp.J;
     const long long J1 = J + 1;
@@ -371,241 +378,294 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
     }
 
     __syncthreads();  // statistics part zeroed, table staged
-    // Lanes past the last trajectory stay in the warp-uniform loop as idle
-    // lanes (their loads use a valid trajectory id; they never record).
-    const bool in_range = slot < rp.n_launch;
-    const long long g = launch_traj(rp, in_range ? slot : rp.n_launch - 1);  // trajectory of the lane
-    const long long gc = g;
     {
-        const long long p = gc / rp.R;
-        const long long cell_base = (p - p_base) * J1 * O;
-        const uint64_t gk = (uint64_t)global_traj(gc, rp.R, rp.R_total, rp.r_off);  // RNG stream id
-        int tslot = -1;
-        double *trace = nullptr;
-        long long tn_rec = 0;
-        if (TRACE && in_range) {
-            for (int i = 0; i < rp.n_trace; ++i)
-                if (rp.trace_g[i] == g) tslot = i;
-            if (tslot >= 0) trace = rp.trace_buf + (long long)tslot * rp.trace_cap * 5;
+        // per-trajectory state (index i < NT); lanes past the last trajectory
+        // stay in the warp-uniform loop as idle lanes (their loads use a valid
+        // trajectory id; they never record)
+        bool in_range[NT];
+        long long g[NT], cell_base[NT];
+        uint64_t gk[NT];
+        int tslot[NT];
+        double *trace[NT];
+        long long tn_rec[NT];
+        int x[NT][S];
+        double t[NT];
+        long long j[NT];
+        unsigned long long n[NT], n_start[NT];
+        double c[NT][M];
+        FastChain<S, M> fc[NT];
+        double t_next[NT], t_next2[NT];
+        long long firings[NT];
+        int status[NT];
+        double Eb[NT][B], Ub[NT][B];
+        bool live[NT];
+        const Gather<S, M> gt(tt);
+        const long long JL = RES ? rp.j_stop - 1 : J;  // last sample of this launch (J in one-shot runs)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+            const long long slot = g0 + (long long)threadIdx.x * NT + i;
+            in_range[i] = slot < rp.n_launch;
+            g[i] = launch_traj(rp, in_range[i] ? slot : rp.n_launch - 1);
+            const long long p = g[i] / rp.R;
+            cell_base[i] = (p - p_base) * J1 * O;
+            gk[i] = (uint64_t)global_traj(g[i], rp.R, rp.R_total, rp.r_off);  // RNG stream id
+            tslot[i] = -1;
+            trace[i] = nullptr;
+            tn_rec[i] = 0;
+            if (TRACE && in_range[i]) {
+                for (int q = 0; q < rp.n_trace; ++q)
+                    if (rp.trace_g[q] == g[i]) tslot[i] = q;
+                if (tslot[i] >= 0) trace[i] = rp.trace_buf + (long long)tslot[i] * rp.trace_cap * 5;
+            }
+            // state: fresh (x0, t = 0, n = 0, j = 0) or resumed (cwc_run_advance)
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                x[i][s] = (s < tt.n_cells) ? (RES ? rp.rs_x[g[i] * tt.n_cells + s] : tt.init[s]) : 0;
+            t[i] = 0.0;
+            j[i] = 0;
+            n[i] = 0;
+            if (RES) {
+                t[i] = rp.rs_t[g[i]];
+                j[i] = rp.rs_j[g[i]];
+                n[i] = (unsigned long long)rp.rs_n[g[i]];
+            }
+            n_start[i] = n[i];
+#pragma unroll
+            for (int m = 0; m < M; ++m) c[i][m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
+            fc[i].rates(tt, c[i]);
+            fc[i].load(tt, x[i]);
+            t_next[i] = __dmul_rn(__ll2double_rn(j[i]), rp.dt);       // j * dt (fresh: sample 0 is crossed by the first firing)
+            t_next2[i] = __dmul_rn(__ll2double_rn(j[i] + 1), rp.dt);  // (j + 1) * dt
+            firings[i] = (long long)n[i];
+            status[i] = CWC_TRAJ_DONE;
+#pragma unroll
+            for (int q = 0; q < B; ++q) block_to_draws(philox_block(rp.seed, gk[i], n[i] + q), Eb[i][q], Ub[i][q]);
+            live[i] = in_range[i] && j[i] <= JL;
         }
-        auto trace_rec = [&](unsigned long long n_, double a0, double tau, double tn, int mu) {
-            if (TRACE && tslot >= 0 && tn_rec < rp.trace_cap) {
-                double *r = trace + 5 * tn_rec++;
+        auto trace_rec = [&](int i, unsigned long long n_, double a0, double tau, double tn, int mu) {
+            if (TRACE && tslot[i] >= 0 && tn_rec[i] < rp.trace_cap) {
+                double *r = trace[i] + 5 * tn_rec[i]++;
                 r[0] = (double)n_; r[1] = a0; r[2] = tau; r[3] = tn; r[4] = (double)mu;
             }
         };
-
-        // state: fresh (x0, t = 0, n = 0, j = 0) or resumed (cwc_run_advance)
-        int x[S];
+        auto any_live = [&]() {
+            bool l = false;
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            x[s] = (s < tt.n_cells) ? (RES ? rp.rs_x[g * tt.n_cells + s] : tt.init[s]) : 0;
-        double t = 0.0;
-        long long j = 0;
-        unsigned long long n = 0;
-        if (RES) {
-            t = rp.rs_t[g];
-            j = rp.rs_j[g];
-            n = (unsigned long long)rp.rs_n[g];
-        }
-        const long long JL = RES ? rp.j_stop - 1 : J;  // last sample of this launch (J in one-shot runs)
-        const unsigned long long n_start = n;
-        double c[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) c[m] = (m < tt.M) ? __ldg(rp.rates + p * tt.M + m) : 0.0;
-        const Gather<S, M> gt(tt);
-        FastChain<S, M> fc;
-        fc.rates(tt, c);
-        fc.load(tt, x);
+            for (int i = 0; i < NT; ++i) l = l || live[i];
+            return l;
+        };
 
-        double t_next = __dmul_rn(__ll2double_rn(j), rp.dt);  // j * dt (fresh: sample 0 is crossed by the first firing)
-        double t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);  // (j + 1) * dt
-        long long firings = (long long)n;
-        int status = CWC_TRAJ_DONE;
-        double Eb[B], Ub[B];
-#pragma unroll
-        for (int i = 0; i < B; ++i) block_to_draws(philox_block(rp.seed, gk, n + i), Eb[i], Ub[i]);
-
-        bool live = in_range && j <= JL;
-        while (__any_sync(0xffffffffu, live)) {
-            // ---- fast batch: B firings run speculatively (every step commits
-            // its update); the four phases of the next batch's draws
-            // (n0+B .. n0+2B-1, valid if all B firings turn out plain) are
-            // interleaved with the steps so that the scheduler can overlap
-            // their independent chains with the serial state chain ----
-            const unsigned long long n0 = n;
-            double En[B], Un[B];
-            DrawPipe<B> pipe;
-            pipe.start(gk, n0 + B);
-            int xsnap[B][S];
-            double tsnap[B];
-            unsigned bad = 0;  // bit k: firing k of the batch is not plain
+        while (__any_sync(0xffffffffu, any_live())) {
+            // ---- fast batch: B firings of every trajectory of the lane run
+            // speculatively (every step commits its update); the four phases
+            // of the next batch's draws (n0+B .. n0+2B-1, valid if all B
+            // firings turn out plain) are interleaved with the steps so that
+            // the scheduler can overlap their independent chains with the
+            // serial state chains ----
+            unsigned long long n0[NT];
+            double En[NT][B], Un[NT][B];
+            DrawPipe<B> pipe[NT];
+            int xsnap[NT][B][S];
+            double tsnap[NT][B];
+            unsigned bad[NT];  // bit k: firing k of the batch is not plain
             // one firing per batch may cross a single sample time that is not
             // the last: it commits, its record (pre-event state) follows the batch
             // (at most one: it is the batch's only change of j, so the
             // per-firing bookkeeping is a few selects; the batch-start sample
             // times are kept for a rollback, and t_next3 = (j + 2) dt becomes
             // the next-but-one sample time after the crossing)
-            bool rec = false;
-            int krec = B;
-            const bool jok = j < JL;
-            const double t_next0 = t_next, t_next20 = t_next2;
-            const double t_next3 = __dmul_rn(__ll2double_rn(j + 2), rp.dt);
-            FireRec fr[B];
+            bool rec[NT];
+            int krec[NT];
+            bool jok[NT];
+            double t_next0[NT], t_next20[NT], t_next3[NT];
+            FireRec fr[NT][B];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                n0[i] = n[i];
+                pipe[i].start(gk[i], n0[i] + B);
+                bad[i] = 0;
+                rec[i] = false;
+                krec[i] = B;
+                jok[i] = j[i] < JL;
+                t_next0[i] = t_next[i];
+                t_next20[i] = t_next2[i];
+                t_next3[i] = __dmul_rn(__ll2double_rn(j[i] + 2), rp.dt);
+            }
 #pragma unroll
             for (int k = 0; k < B; ++k) {
 #pragma unroll
                 for (int ph = 0; ph < 4; ++ph)
-                    if ((ph * B) / 4 == k) pipe.phase(ph, rp.seed, ltab, En, Un);
+                    if ((ph * B) / 4 == k) {
 #pragma unroll
-                for (int s = 0; s < S; ++s) xsnap[k][s] = x[s];
-                tsnap[k] = t;
-                bool cross1;
-                const bool plain = fc.template step2<TRACE>(tt, gt, c, x, t, Eb[k], Ub[k], t_next, t_next2, cross1, fr[k]);
-                const bool take = cross1 && !rec && jok;
-                rec = rec || take;
-                krec = take ? k : krec;
-                t_next = take ? t_next2 : t_next;
-                t_next2 = take ? t_next3 : t_next2;
-                bad |= (plain || take) ? 0u : (1u << k);
-            }
-            if (!live) bad = 1u;
-            const int used = (bad == 0u) ? B : __ffs(bad) - 1;  // plain firings committed
-            if (TRACE && live) {  // trace records of the committed speculative firings
+                        for (int i = 0; i < NT; ++i) pipe[i].phase(ph, rp.seed, ltab, En[i], Un[i]);
+                    }
 #pragma unroll
-                for (int k = 0; k < B; ++k)
-                    if (k < used) trace_rec(n0 + k, fr[k].a0, fr[k].tau, fr[k].tn, fr[k].mu);
+                for (int i = 0; i < NT; ++i) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s) xsnap[i][k][s] = x[i][s];
+                    tsnap[i][k] = t[i];
+                    bool cross1;
+                    const bool plain = fc[i].template step2<TRACE>(tt, gt, c[i], x[i], t[i], Eb[i][k], Ub[i][k], t_next[i],
+                                                                   t_next2[i], cross1, fr[i][k]);
+                    const bool take = cross1 && !rec[i] && jok[i];
+                    rec[i] = rec[i] || take;
+                    krec[i] = take ? k : krec[i];
+                    t_next[i] = take ? t_next2[i] : t_next[i];
+                    t_next2[i] = take ? t_next3[i] : t_next2[i];
+                    bad[i] |= (plain || take) ? 0u : (1u << k);
+                }
             }
-            if (rec && krec >= used) {  // the crossing firing was rolled back
-                rec = false;
-                t_next = t_next0;
-                t_next2 = t_next20;
-            }
-            const long long jrec = j;  // the sample a committed crossing recorded
-            if (rec) j += 1;
-            if (live) {
-                n += (unsigned long long)used;
-                firings += used;
+            long long jrec[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) {
+                if (!live[i]) bad[i] = 1u;
+                const int used = (bad[i] == 0u) ? B : __ffs(bad[i]) - 1;  // plain firings committed
+                if (TRACE && live[i]) {  // trace records of the committed speculative firings
+#pragma unroll
+                    for (int k = 0; k < B; ++k)
+                        if (k < used) trace_rec(i, n0[i] + k, fr[i][k].a0, fr[i][k].tau, fr[i][k].tn, fr[i][k].mu);
+                }
+                if (rec[i] && krec[i] >= used) {  // the crossing firing was rolled back
+                    rec[i] = false;
+                    t_next[i] = t_next0[i];
+                    t_next2[i] = t_next20[i];
+                }
+                jrec[i] = j[i];  // the sample a committed crossing recorded
+                if (rec[i]) j[i] += 1;
+                if (live[i]) {
+                    n[i] += (unsigned long long)used;
+                    firings[i] += used;
+                }
             }
             // records staged in shared memory, written 32 at a time (one per lane)
-            const unsigned rmask = __ballot_sync(0xffffffffu, rec);
-            if (rmask) {
-                if (rec) {  // few lanes: stage the counts only, observables are formed at the flush
-                    const int slot = stage_n + __popc(rmask & ((1u << lane) - 1u));
-                    st_cell[slot] = cell_base + jrec * O;
-                    st_row[slot] = g * J1 + jrec;
 #pragma unroll
-                    for (int k = 0; k < B; ++k)  // pre-event counts of firing krec
-                        if (k == krec) {
+            for (int i = 0; i < NT; ++i) {
+                const unsigned rmask = __ballot_sync(0xffffffffu, rec[i]);
+                if (rmask) {
+                    if (rec[i]) {  // few lanes: stage the counts only, observables are formed at the flush
+                        const int sl = stage_n + __popc(rmask & ((1u << lane) - 1u));
+                        st_cell[sl] = cell_base[i] + jrec[i] * O;
+                        st_row[sl] = g[i] * J1 + jrec[i];
 #pragma unroll
-                            for (int s = 0; s < S; ++s) st_x[slot * kThreadMaxCells + s] = xsnap[k][s];
-                        }
-                }
-                stage_n += __popc(rmask);
-                if (stage_n >= 32) {
-                    __syncwarp();
-                    const int e = stage_n - 32 + lane;
-                    staged_record<S>(rp, tt, acc, st_cell[e], st_row[e], st_x + e * kThreadMaxCells);
-                    stage_n -= 32;
-                    __syncwarp();
+                        for (int k = 0; k < B; ++k)  // pre-event counts of firing krec
+                            if (k == krec[i]) {
+#pragma unroll
+                                for (int s = 0; s < S; ++s) st_x[sl * kThreadMaxCells + s] = xsnap[i][k][s];
+                            }
+                    }
+                    stage_n += __popc(rmask);
+                    if (stage_n >= 32) {
+                        __syncwarp();
+                        const int e = stage_n - 32 + lane;
+                        staged_record<S>(rp, tt, acc, st_cell[e], st_row[e], st_x + e * kThreadMaxCells);
+                        stage_n -= 32;
+                        __syncwarp();
+                    }
                 }
             }
 
             // ---- rare: roll back to the first non-plain firing, run ONE exact
             // iteration (the oracle's loop body) and shift the draws ----
-            if (__any_sync(0xffffffffu, bad != 0u)) {
-                bool fill = false;  // stalled here: samples j .. JL filled below, warp-wide
-                double E = Eb[0], u2 = Ub[0];  // draw of firing n (= batch slot `used`)
-                if (bad != 0u) {
 #pragma unroll
-                    for (int k = 0; k < B; ++k) {
-                        if (k == used) {
+            for (int i = 0; i < NT; ++i) {
+                if (__any_sync(0xffffffffu, bad[i] != 0u)) {
+                    bool fill = false;  // stalled here: samples j .. JL filled below, warp-wide
+                    double E = Eb[i][0], u2 = Ub[i][0];  // draw of firing n (= batch slot `used`)
+                    const int used = (bad[i] == 0u) ? B : __ffs(bad[i]) - 1;
+                    if (bad[i] != 0u) {
 #pragma unroll
-                            for (int s = 0; s < S; ++s) x[s] = xsnap[k][s];
-                            t = tsnap[k];
-                            E = Eb[k];
-                            u2 = Ub[k];
-                        }
-                    }
-                }
-                if (live && bad != 0u) {
-                    double cum[M];
-                    cumulative(tt, gt, x, c, cum);
-                    const double a0 = cum[M - 1];
-                    if (a0 == 0.0) {  // stall: no draw is consumed
-                        fill = true;
-                        status = CWC_TRAJ_STALLED;
-                        live = false;
-                    } else {
-                        const double tau = __ddiv_rn(E, a0);
-                        const double tn = __dadd_rn(t, tau);
-                        while (j <= JL && __dmul_rn(__ll2double_rn(j), rp.dt) <= tn) {
-                            record_sample(rp, tt, acc, x, cell_base, g, j);
-                            ++j;
-                        }
-                        if (j > JL) {  // horizon (or the launch's last sample) reached: drawn, not applied
-                            trace_rec(n, a0, tau, tn, -1);
-                            status = CWC_TRAJ_DONE;
-                            live = false;
-                        } else {
-                            t_next = __dmul_rn(__ll2double_rn(j), rp.dt);
-                            t_next2 = __dmul_rn(__ll2double_rn(j + 1), rp.dt);
-                            int mu;
-                            const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
-                            int xn[S];
-                            trace_rec(n, a0, tau, tn, mu);  // (the oracle records an overflowing firing too)
-                            if (apply_nu(x, nu, xn)) {  // a count would leave int32: freeze + fill
-                                for (; j <= JL; ++j) record_sample(rp, tt, acc, x, cell_base, g, j);
-                                status = CWC_TRAJ_OVERFLOW;
-                                live = false;
-                            } else {
+                        for (int k = 0; k < B; ++k) {
+                            if (k == used) {
 #pragma unroll
-                                for (int s = 0; s < S; ++s) x[s] = xn[s];
-                                t = tn;
-                                ++n;
-                                ++firings;
+                                for (int s = 0; s < S; ++s) x[i][s] = xsnap[i][k][s];
+                                t[i] = tsnap[i][k];
+                                E = Eb[i][k];
+                                u2 = Ub[i][k];
                             }
                         }
                     }
-                    if (live) {
-                        // draws of firings n .. n+B-1 are slots [u, u+B) of
-                        // (this batch ++ next batch), u = n - n0 in [1, B]
-                        const int u = (int)(n - n0);
-                        double E2[B], U2[B];
+                    if (live[i] && bad[i] != 0u) {
+                        double cum[M];
+                        cumulative(tt, gt, x[i], c[i], cum);
+                        const double a0 = cum[M - 1];
+                        if (a0 == 0.0) {  // stall: no draw is consumed
+                            fill = true;
+                            status[i] = CWC_TRAJ_STALLED;
+                            live[i] = false;
+                        } else {
+                            const double tau = __ddiv_rn(E, a0);
+                            const double tn = __dadd_rn(t[i], tau);
+                            while (j[i] <= JL && __dmul_rn(__ll2double_rn(j[i]), rp.dt) <= tn) {
+                                record_sample(rp, tt, acc, x[i], cell_base[i], g[i], j[i]);
+                                ++j[i];
+                            }
+                            if (j[i] > JL) {  // horizon (or the launch's last sample) reached: drawn, not applied
+                                trace_rec(i, n[i], a0, tau, tn, -1);
+                                status[i] = CWC_TRAJ_DONE;
+                                live[i] = false;
+                            } else {
+                                t_next[i] = __dmul_rn(__ll2double_rn(j[i]), rp.dt);
+                                t_next2[i] = __dmul_rn(__ll2double_rn(j[i] + 1), rp.dt);
+                                int mu;
+                                const unsigned long long nu = select_nu<M, TRACE>(tt, cum, __dmul_rn(u2, a0), mu);
+                                int xn[S];
+                                trace_rec(i, n[i], a0, tau, tn, mu);  // (the oracle records an overflowing firing too)
+                                if (apply_nu(x[i], nu, xn)) {  // a count would leave int32: freeze + fill
+                                    for (; j[i] <= JL; ++j[i]) record_sample(rp, tt, acc, x[i], cell_base[i], g[i], j[i]);
+                                    status[i] = CWC_TRAJ_OVERFLOW;
+                                    live[i] = false;
+                                } else {
 #pragma unroll
-                        for (int i = 0; i < B; ++i) {
-                            E2[i] = En[i];
-                            U2[i] = Un[i];
-#pragma unroll
-                            for (int cc = 1; cc < B; ++cc) {
-                                const int src = cc + i;
-                                if (cc == u) {
-                                    E2[i] = src < B ? Eb[src] : En[src - B];
-                                    U2[i] = src < B ? Ub[src] : Un[src - B];
+                                    for (int s = 0; s < S; ++s) x[i][s] = xn[s];
+                                    t[i] = tn;
+                                    ++n[i];
+                                    ++firings[i];
                                 }
                             }
                         }
+                        if (live[i]) {
+                            // draws of firings n .. n+B-1 are slots [u, u+B) of
+                            // (this batch ++ next batch), u = n - n0 in [1, B]
+                            const int u = (int)(n[i] - n0[i]);
+                            double E2[B], U2[B];
 #pragma unroll
-                        for (int i = 0; i < B; ++i) {
-                            En[i] = E2[i];
-                            Un[i] = U2[i];
+                            for (int q = 0; q < B; ++q) {
+                                E2[q] = En[i][q];
+                                U2[q] = Un[i][q];
+#pragma unroll
+                                for (int cc = 1; cc < B; ++cc) {
+                                    const int src = cc + q;
+                                    if (cc == u) {
+                                        E2[q] = src < B ? Eb[i][src] : En[i][src - B];
+                                        U2[q] = src < B ? Ub[i][src] : Un[i][src - B];
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int q = 0; q < B; ++q) {
+                                En[i][q] = E2[q];
+                                Un[i][q] = U2[q];
+                            }
                         }
                     }
-                }
-                if (bad != 0u) fc.load(tt, x);  // x was rolled back / changed
-                const unsigned fm = __ballot_sync(0xffffffffu, fill);
-                if (fm) {
-                    stall_fill<S>(rp, tt, acc, fm, x, cell_base, g, j, JL, lane);
-                    if (fill) j = JL + 1;
+                    if (bad[i] != 0u) fc[i].load(tt, x[i]);  // x was rolled back / changed
+                    const unsigned fm = __ballot_sync(0xffffffffu, fill);
+                    if (fm) {
+                        stall_fill<S>(rp, tt, acc, fm, x[i], cell_base[i], g[i], j[i], JL, lane);
+                        if (fill) j[i] = JL + 1;
+                    }
                 }
             }
 #pragma unroll
-            for (int i = 0; i < B; ++i) {
-                Eb[i] = En[i];
-                Ub[i] = Un[i];
+            for (int i = 0; i < NT; ++i) {
+#pragma unroll
+                for (int q = 0; q < B; ++q) {
+                    Eb[i][q] = En[i][q];
+                    Ub[i][q] = Un[i][q];
+                }
+                // resumable runs: suspend after `quantum` further firings
+                if (RES && rp.quantum > 0 && live[i] && n[i] - n_start[i] >= (unsigned long long)rp.quantum) live[i] = false;
             }
-            // resumable runs: suspend after `quantum` further firings
-            if (RES && rp.quantum > 0 && live && n - n_start >= (unsigned long long)rp.quantum) live = false;
             // reconverge the warp explicitly: the vote at the loop head only
             // synchronises it, and a warp left split after the rare path would
             // run every later batch twice with half its lanes (a plain
@@ -615,18 +675,21 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
         __syncwarp();
         if (lane < stage_n)  // drain the staged records
             staged_record<S>(rp, tt, acc, st_cell[lane], st_row[lane], st_x + lane * kThreadMaxCells);
-        if (in_range) {
-            if (RES && j <= J && status == CWC_TRAJ_DONE) status = CWC_TRAJ_RUNNING;  // suspended
-            if (rp.out_firings) rp.out_firings[g] = firings;
-            if (rp.out_status) rp.out_status[g] = status;
-            if (TRACE && tslot >= 0) rp.trace_len[tslot] = tn_rec;
-            if (RES) {
 #pragma unroll
-                for (int s = 0; s < S; ++s)
-                    if (s < tt.n_cells) rp.rs_x[g * tt.n_cells + s] = x[s];
-                rp.rs_t[g] = t;
-                rp.rs_n[g] = (int64_t)n;
-                rp.rs_j[g] = (int32_t)j;
+        for (int i = 0; i < NT; ++i) {
+            if (in_range[i]) {
+                if (RES && j[i] <= J && status[i] == CWC_TRAJ_DONE) status[i] = CWC_TRAJ_RUNNING;  // suspended
+                if (rp.out_firings) rp.out_firings[g[i]] = firings[i];
+                if (rp.out_status) rp.out_status[g[i]] = status[i];
+                if (TRACE && tslot[i] >= 0) rp.trace_len[tslot[i]] = tn_rec[i];
+                if (RES) {
+#pragma unroll
+                    for (int s = 0; s < S; ++s)
+                        if (s < tt.n_cells) rp.rs_x[g[i] * tt.n_cells + s] = x[i][s];
+                    rp.rs_t[g[i]] = t[i];
+                    rp.rs_n[g[i]] = (int64_t)n[i];
+                    rp.rs_j[g[i]] = (int32_t)j[i];
+                }
             }
         }
     }
@@ -654,23 +717,21 @@ cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, 
         k<<<(unsigned)((rp.G + 32 * kWsGroups - 1) / (32 * kWsGroups)), 32 * (1 + kWsProducers) * kWsGroups, smem, st>>>(rp, tt);
         return cudaGetLastError();
     }
-    if (rp.rs_x) {  // resumable runs (never traced)
-        auto k = ssa_thread_kernel<S, M, false, true>;
+    // two trajectories per lane (rp.thread_nt == 2) only for one-shot runs of
+    // models with 4-firing batches (M <= 8)
+    constexpr bool NT2 = ThreadBatch<M>::B >= 2;
+    const bool nt2 = NT2 && rp.thread_nt == 2 && !rp.rs_x;
+    const long long blocks2 = (rp.n_launch + 2ll * threads - 1) / (2ll * threads);
+    auto go = [&](auto k, long long nb) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);
-    } else if (trace) {
-        auto k = ssa_thread_kernel<S, M, true, false>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);
-    } else {
-        auto k = ssa_thread_kernel<S, M, false, false>;
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        k<<<(unsigned)blocks, threads, smem, st>>>(rp, tt);
-    }
-    return cudaGetLastError();
+        k<<<(unsigned)nb, threads, smem, st>>>(rp, tt);
+        return cudaGetLastError();
+    };
+    if (rp.rs_x) return go(ssa_thread_kernel<S, M, false, true, 1>, blocks);  // resumable runs (never traced)
+    if (nt2) return trace ? go(ssa_thread_kernel<S, M, true, false, NT2 ? 2 : 1>, blocks2)
+                          : go(ssa_thread_kernel<S, M, false, false, NT2 ? 2 : 1>, blocks2);
+    return trace ? go(ssa_thread_kernel<S, M, true, false, 1>, blocks) : go(ssa_thread_kernel<S, M, false, false, 1>, blocks);
 }
 
 template <int S>
