@@ -57,12 +57,13 @@ enum { CWC_PATH_AUTO = -1, CWC_PATH_THREAD = 0, CWC_PATH_WARP = 1 };
    choice.  THREAD_WS: warp-specialised producer/consumer thread kernel;
    THREAD: single-warp batched thread kernel, one trajectory per lane;
    THREAD2: the same kernel with two trajectories per lane (M <= 8, one-shot
-   runs); WARP2: two trajectories per warp (16-lane segments, M <= 256);
+   runs); THREAD_WS2: warp-specialised with two trajectories per consumer
+   lane (M <= 8, one-shot runs); WARP2: two trajectories per warp (16-lane segments, M <= 256);
    WARP: one trajectory per warp.  Every
    variant computes the same trajectories (up to the traced a0-sum-order
    class between the thread and warp families). */
 enum { CWC_KERNEL_AUTO = 0, CWC_KERNEL_THREAD_WS = 1, CWC_KERNEL_THREAD = 2, CWC_KERNEL_WARP2 = 3,
-       CWC_KERNEL_WARP = 4, CWC_KERNEL_THREAD2 = 5 };
+       CWC_KERNEL_WARP = 4, CWC_KERNEL_THREAD2 = 5, CWC_KERNEL_THREAD_WS2 = 6 };
 
 /* Where the on-line moments accumulate (cwc_sim_opts.stats_mode): per-CTA
    shared-memory parts flushed to global memory, or one global part updated

@@ -521,12 +521,13 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     const int smode = opts ? opts->stats_mode : CWC_STATS_AUTO;
     const int wpb = opts ? opts->warps_per_block : 0;
     const int bps = opts ? opts->blocks_per_sm : 0;
-    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_THREAD2) return fail(CWC_ERR_INVALID, "bad kernel");
+    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_THREAD_WS2) return fail(CWC_ERR_INVALID, "bad kernel");
     if (smode < CWC_STATS_AUTO || smode > CWC_STATS_GLOBAL) return fail(CWC_ERR_INVALID, "bad stats_mode");
     if (wpb < 0 || wpb > 4) return fail(CWC_ERR_INVALID, "warps_per_block must be in [0, 4]");
     if (bps < 0 || bps > 32) return fail(CWC_ERR_INVALID, "blocks_per_sm must be in [0, 32]");
     if (force != CWC_PATH_AUTO && force != CWC_PATH_THREAD && force != CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "bad force_path");
-    if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD || kern == CWC_KERNEL_THREAD2) {
+    if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD || kern == CWC_KERNEL_THREAD2 ||
+        kern == CWC_KERNEL_THREAD_WS2) {
         if (force == CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_THREAD;
     } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP) {
@@ -565,6 +566,18 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // table-driven log: C2 at 16384 replicas 8.58e10 vs 8.41e10
         // firings/s; one lone CTA 274 vs 355 cycles per firing)
         bool ws = !bt && (pl.G + 31) / 32 <= 2ll * nsm;
+        // two trajectories per consumer lane (ssa_thread_ws2.cuh) only on
+        // request: measured 2x slower per trajectory on C2 (a consumer with
+        // two interleaved chains takes ~650 cycles per firing pair, against
+        // ~290 per firing with one: the consumer is throughput-, not
+        // latency-bound), with one or two producer warps alike
+        int ws2 = 0;
+        if (kern == CWC_KERNEL_THREAD_WS2) {
+            if (resumable || bt || pl.m_pad > 8)
+                return fail(CWC_ERR_INVALID, "kernel THREAD_WS2 needs M <= 8, a one-shot run and no block_threads");
+            ws2 = 1;
+        }
+        if (ws2) ws = true;
         if (kern == CWC_KERNEL_THREAD_WS) {
             if (resumable) return fail(CWC_ERR_INVALID, "resumable runs do not use the warp-specialised kernel");
             if (bt && bt != 32 * kWsGroups) return fail(CWC_ERR_INVALID, "the warp-specialised kernel has a fixed CTA shape (block_threads)");
@@ -573,8 +586,9 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             ws = false;
         }
         if (resumable) ws = false;
-        if (ws) T = 32 * kWsGroups;
-        pl.ws = ws ? 1 : 0;
+        if (kern == CWC_KERNEL_THREAD_WS || kern == CWC_KERNEL_THREAD) ws2 = 0;
+        if (ws) T = ws2 ? 64 : 32 * kWsGroups;
+        pl.ws = ws ? (ws2 ? 2 : 1) : 0;
         pl.threads = T;
         // single-warp kernel: two trajectories per lane (ssa_thread_impl.cuh
         // NT) only on request -- measured 3x slower on C2/C3 (the doubled
@@ -582,7 +596,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         pl.nt = (!ws && !resumable && pl.m_pad <= 8 && kern == CWC_KERNEL_THREAD2) ? 2 : 1;
         if (kern == CWC_KERNEL_THREAD2 && pl.nt != 2)
             return fail(CWC_ERR_INVALID, "kernel THREAD2 needs M <= 8 and a one-shot run");
-        const int64_t blocks = (NL + (int64_t)T * pl.nt - 1) / ((int64_t)T * pl.nt);
+        const int64_t blocks = (NL + (int64_t)T * pl.nt - 1) / ((int64_t)T * pl.nt);  // (ws2: T = 64 trajectories)
         if (blocks > 0x7fffffffll) return fail(CWC_ERR_INVALID, "too many trajectories for one launch");
         pl.blocks = (int)blocks;
         // points touched by one block
@@ -598,7 +612,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         const size_t smem = (size_t)stat_bytes(lay_s, cells);
         // beyond the statistics part: the draw ring + staging of the
         // warp-specialised CTA, or the record staging of each warp
-        const size_t extra = (ws ? kWsRingBytes : (size_t)(T / 32) * kStageLL * sizeof(long long)) + kNegLogSmemBytes;
+        const size_t extra = (ws ? (pl.ws == 2 ? kWs2RingBytes : kWsRingBytes) : (size_t)(T / 32) * kStageLL * sizeof(long long)) +
+                             kNegLogSmemBytes;
         // One global part (fire-and-forget 64-bit REDs to L2) by default:
         // measured faster than per-CTA shared-memory parts on every config
         // (profiles/r02/stats_modes.json: C1 4.60e9 vs 4.17e9, C2 8.95e10 vs
@@ -809,7 +824,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     // per-point rates (and, for sweeps on the thread path, the dispatch
     // order) through the model's pinned staging (cwc_model_s::Stage)
     const bool want_order = pl.path == CWC_PATH_THREAD && pl.P > 1;
-    const int T_order = pl.ws ? 32 * kWsGroups : pl.threads * pl.nt;
+    const int T_order = pl.ws == 2 ? 64 : pl.ws ? 32 * kWsGroups : pl.threads * pl.nt;
     cudaError_t e = cudaSuccess;
     {
         uint64_t key = 0xcbf29ce484222325ull;
@@ -1316,11 +1331,15 @@ cwc_status cwc_plan(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, dou
     cwc_status s = plan_run(m, n_replicas, sweep, t_end, sample_dt, opts, false, pl);
     if (s != CWC_OK) return s;
     info->kernel = pl.path == CWC_PATH_THREAD
-                       ? (pl.ws ? CWC_KERNEL_THREAD_WS : (pl.nt == 2 ? CWC_KERNEL_THREAD2 : CWC_KERNEL_THREAD))
+                       ? (pl.ws == 2 ? CWC_KERNEL_THREAD_WS2 : pl.ws ? CWC_KERNEL_THREAD_WS
+                                                                   : (pl.nt == 2 ? CWC_KERNEL_THREAD2 : CWC_KERNEL_THREAD))
                        : (pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
-    info->blocks = pl.path == CWC_PATH_THREAD ? (pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)
-                                              : pl.blocks;
-    info->threads = pl.path == CWC_PATH_THREAD ? (pl.ws ? 32 * (1 + kWsProducers) * kWsGroups : pl.threads) : pl.threads;
+    info->blocks = pl.path == CWC_PATH_THREAD
+                       ? (pl.ws == 2 ? (int32_t)((pl.G + 63) / 64)
+                                     : pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)
+                       : pl.blocks;
+    info->threads = pl.path == CWC_PATH_THREAD ? (pl.ws == 2 ? 32 * (1 + kWs2Producers) : pl.ws ? 32 * (1 + kWsProducers) * kWsGroups : pl.threads)
+                                               : pl.threads;
     info->stats_shared = pl.stats_smem;
     info->smem_bytes = (int64_t)pl.smem_bytes;
     info->n_parts = pl.n_parts;

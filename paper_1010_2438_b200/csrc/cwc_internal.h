@@ -68,6 +68,16 @@ constexpr size_t kWsGroupBytes = (size_t)2 * kWsRing * 32 * sizeof(double) +
 // staging longs per warp: per record its first cell, its dump row, its counts (int32)
 constexpr long long kStageLL = (long long)kWsStage * (2 + kThreadMaxCells / 2);
 constexpr size_t kWsRingBytes = kWsGroups * ((kWsGroupBytes + 15) & ~(size_t)15);  // per CTA
+// two trajectories per consumer lane (ssa_thread_ws2.cuh), served by 1
+// producer warp (both trajectories of each lane) or 2 (one slot each)
+#ifndef CWC_WS2_PRODUCERS
+#define CWC_WS2_PRODUCERS 2
+#endif
+constexpr int kWs2Producers = CWC_WS2_PRODUCERS;
+// rings of 64
+// trajectories, per-trajectory counters, the staging of one consumer warp
+constexpr size_t kWs2RingBytes = (((size_t)2 * kWsRing * 64 * sizeof(double) + (size_t)3 * 64 * sizeof(unsigned) +
+                                   (size_t)kWsStage * (2 + kThreadMaxCells / 2) * sizeof(long long)) + 15) & ~(size_t)15;
 // shared-memory copy of the -log reduction table (device_common.cuh,
 // neglog_table.h) in the thread kernels: {T, L_hi} pairs then L_lo
 struct NegLogSmem {

@@ -546,12 +546,15 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                         const int sl = stage_n + __popc(rmask & ((1u << lane) - 1u));
                         st_cell[sl] = cell_base[i] + jrec[i] * O;
                         st_row[sl] = g[i] * J1 + jrec[i];
+                        // pre-event counts of firing krec, by selects (no dynamic
+                        // indexing of register arrays: local memory otherwise)
 #pragma unroll
-                        for (int k = 0; k < B; ++k)  // pre-event counts of firing krec
-                            if (k == krec[i]) {
+                        for (int s = 0; s < S; ++s) {
+                            int v = xsnap[i][0][s];
 #pragma unroll
-                                for (int s = 0; s < S; ++s) st_x[sl * kThreadMaxCells + s] = xsnap[i][k][s];
-                            }
+                            for (int k = 1; k < B; ++k) v = (k == krec[i]) ? xsnap[i][k][s] : v;
+                            st_x[sl * kThreadMaxCells + s] = v;
+                        }
                     }
                     stage_n += __popc(rmask);
                     if (stage_n >= 32) {
@@ -572,16 +575,21 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                     bool fill = false;  // stalled here: samples j .. JL filled below, warp-wide
                     double E = Eb[i][0], u2 = Ub[i][0];  // draw of firing n (= batch slot `used`)
                     const int used = (bad[i] == 0u) ? B : __ffs(bad[i]) - 1;
-                    if (bad[i] != 0u) {
+                    if (bad[i] != 0u) {  // roll back to firing `used` (selects, see above)
+                        double tt0 = tsnap[i][0];
 #pragma unroll
-                        for (int k = 0; k < B; ++k) {
-                            if (k == used) {
+                        for (int k = 1; k < B; ++k) {
+                            tt0 = (k == used) ? tsnap[i][k] : tt0;
+                            E = (k == used) ? Eb[i][k] : E;
+                            u2 = (k == used) ? Ub[i][k] : u2;
+                        }
+                        t[i] = tt0;
 #pragma unroll
-                                for (int s = 0; s < S; ++s) x[i][s] = xsnap[i][k][s];
-                                t[i] = tsnap[i][k];
-                                E = Eb[i][k];
-                                u2 = Ub[i][k];
-                            }
+                        for (int s = 0; s < S; ++s) {
+                            int v = xsnap[i][0][s];
+#pragma unroll
+                            for (int k = 1; k < B; ++k) v = (k == used) ? xsnap[i][k][s] : v;
+                            x[i][s] = v;
                         }
                     }
                     if (live[i] && bad[i] != 0u) {
@@ -705,11 +713,23 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
 
 template <int S, int M, bool TRACE>
 __global__ void ssa_thread_ws_kernel(const RunParams rp, const ThreadTables tt);
+template <int S, int M, bool TRACE>
+__global__ void ssa_thread_ws2_kernel(const RunParams rp, const ThreadTables tt);
 
 template <int S, int M>
 cudaError_t launch_sm(const RunParams &rp, const ThreadTables &tt, int threads, size_t smem, cudaStream_t st,
                       bool trace) {
     const long long blocks = (rp.n_launch + threads - 1) / threads;
+    if (rp.ws == 2) {  // warp-specialised, 64 trajectories per 2-warp CTA (ssa_thread_ws2.cuh)
+        if constexpr (ThreadBatch<M>::B >= 2) {
+            auto k = trace ? ssa_thread_ws2_kernel<S, M, true> : ssa_thread_ws2_kernel<S, M, false>;
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            k<<<(unsigned)((rp.G + 63) / 64), 32 * (1 + kWs2Producers), smem, st>>>(rp, tt);
+            return cudaGetLastError();
+        }
+        return cudaErrorInvalidValue;
+    }
     if (rp.ws) {  // warp-specialised: 32 trajectories per 2-warp CTA (ssa_thread_ws.cuh)
         auto k = trace ? ssa_thread_ws_kernel<S, M, true> : ssa_thread_ws_kernel<S, M, false>;
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -2,6 +2,7 @@
 // (split per cell count so the variants compile in parallel).
 #include "ssa_thread_impl.cuh"
 #include "ssa_thread_ws.cuh"
+#include "ssa_thread_ws2.cuh"
 
 namespace cwc {
 template cudaError_t launch_s<4>(int, const RunParams &, const ThreadTables &, int, size_t, cudaStream_t, bool);

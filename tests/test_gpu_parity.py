@@ -126,6 +126,7 @@ SMALL = [
 KERNELS = [("thread", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS}),  # warp-specialised thread kernel
            ("thread1", cwc.CWC_PATH_THREAD, {"block_threads": 64, "kernel": cwc.CWC_KERNEL_THREAD}),  # single-warp, 1/lane
            ("thread2", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD2}),  # single-warp, 2 trajectories per lane
+           ("ws2", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS2}),   # warp-specialised, 2 per lane
            ("warp", cwc.CWC_PATH_WARP, {}),                           # two trajectories per warp (M <= 256)
            ("warp32", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP})]  # one trajectory per warp
 
@@ -136,7 +137,7 @@ def test_small_parity_full_oracle(name, make, cfg, kname, path, kw):
     kw = dict(kw)
     if name in ("cwc130", "cwc260", "lv16") and path == cwc.CWC_PATH_THREAD:
         pytest.skip("more than 8 cells: warp path only")
-    if name in ("rnd12", "rnd24") and kname == "thread2":
+    if name in ("rnd12", "rnd24") and kname in ("thread2", "ws2"):
         pytest.skip("two trajectories per lane: M <= 8 only")
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
@@ -234,7 +235,8 @@ def test_trace_equals_oracle_trace_thread_path():
         assert cat in ("identical-trace", "log-ulp"), (g, cat, idx, detail)
 
 
-@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_THREAD_WS, cwc.CWC_KERNEL_THREAD, cwc.CWC_KERNEL_THREAD2])
+@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_THREAD_WS, cwc.CWC_KERNEL_THREAD, cwc.CWC_KERNEL_THREAD2,
+                                  cwc.CWC_KERNEL_THREAD_WS2])
 def test_traced_thread_kernels_equal_untraced_and_each_other(kern):
     """Trace writes compiled into a thread kernel change nothing it computes,
     and both thread kernels (warp-specialised and single-warp, fast batches
@@ -308,6 +310,8 @@ def test_thread_kernels_agree_bitwise_multiwave(name, R, t_end):
     a = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD_WS)
     b = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD)
     c = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD2)
+    d = _gpu(model, cfg, sweep, kernel=cwc.CWC_KERNEL_THREAD_WS2)
     for k in ("count", "sum", "sumsq", "firings", "status"):
         assert torch.equal(a[k], b[k]), k
         assert torch.equal(a[k], c[k]), k
+        assert torch.equal(a[k], d[k]), k
