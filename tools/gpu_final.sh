@@ -22,5 +22,14 @@ done
 # counters per config, per-source-line tables, and only the default config's report
 python tools/ncu_summary.py $OUT/ncu_full_summary.json $(for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && echo $c=$OUT/full_$c.ncu-rep; done) > $OUT/ncu_summary.log 2>&1; echo summary=$?
 for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && python tools/ncu_lines.py $OUT/full_$c.ncu-rep 60 > $OUT/lines_$c.txt 2>&1; done
+# dump mode: DRAM bytes of the SSA kernel with and without the trajectory dump (write amplification)
+for c in C2 C4; do
+  python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} --dump > $OUT/dumpcase_$c.log 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ssa_ -c 1 --csv \
+      --log-file $OUT/dump_dram_$c.csv python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} --dump > $OUT/dumpncu_$c.log 2>&1; echo dump_$c=$?
+  python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} > $OUT/nodumpcase_$c.log 2>&1 && \
+  ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:ssa_ -c 1 --csv \
+      --log-file $OUT/nodump_dram_$c.csv python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} > $OUT/nodumpncu_$c.log 2>&1; echo nodump_$c=$?
+done
 mkdir -p $OUT/../reps_${TAG:-final}
 for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ "$c" != "C2" ] && rm -f $OUT/full_$c.ncu-rep; done

@@ -22,6 +22,7 @@ ap.add_argument("--replicas", type=int, default=None)
 ap.add_argument("--path", default="auto", choices=["auto", "thread", "warp"])
 ap.add_argument("--block-threads", type=int, default=0)
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--dump", action="store_true", help="also write every trajectory sample (out_traj)")
 a = ap.parse_args()
 desc, sweep, cfg = wl.config(a.config)
 if a.t_end:
@@ -35,7 +36,7 @@ for k in range(a.repeat):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     out = cwc.simulate(model, cfg["n_replicas"], cfg["t_end"], cfg["sample_dt"], cfg["seed"], sweep=sweep,
-                       force_path=path, block_threads=a.block_threads, buffers=buf)
+                       force_path=path, block_threads=a.block_threads, buffers=buf, want_traj=a.dump)
     e1.record()
     torch.cuda.synchronize()
     buf = out
