@@ -14,6 +14,8 @@ desc, sweep, cfg = w.config("C3")
 model = cwc.cwc_model_create(desc)
 s = torch.cuda.current_stream()
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+for e in ev:
+    e.record()  # torch creates the CUDA event at the first record; the library re-records them
 buf = None
 for it in range(5):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

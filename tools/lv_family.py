@@ -20,6 +20,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import workloads as wl  # noqa: E402
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks during the timed runs)
 from paper_1010_2438_b200 import cwc  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -33,10 +34,13 @@ for n in (2, 4, 8, 16, 32):
     kernels = []
     if model.info.thread_path_ok:
         kernels.append(("thread_ws", cwc.CWC_PATH_THREAD, cwc.CWC_KERNEL_THREAD_WS))
+        kernels.append(("thread", cwc.CWC_PATH_THREAD, cwc.CWC_KERNEL_THREAD))
     if (model.info.n_reactions + 15) // 16 <= 16:
         kernels.append(("warp2", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP2))
     kernels.append(("warp", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP))
     for name, path, kern in kernels:
+        clk = ClockSampler(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
+        clk.start()
         best, buf = None, None
         for k in range(4):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -48,9 +52,10 @@ for n in (2, 4, 8, 16, 32):
             ms = e0.elapsed_time(e1)
             if k > 0:
                 best = ms if best is None else min(best, ms)
+        clocks = clk.stop()
         f = int(out["firings"].sum().item())
         line = {"n_species": n, "reactions": model.info.n_reactions, "kernel": name, "replicas": a.replicas,
-                "t_end": a.t_end, "firings": f, "ms": best, "firings_per_s": f / best * 1e3}
+                "t_end": a.t_end, "firings": f, "ms": best, "firings_per_s": f / best * 1e3, "clocks": clocks}
         print(json.dumps(line), flush=True)
         lines.append(line)
 if a.out:

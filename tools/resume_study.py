@@ -16,6 +16,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import workloads as w  # noqa: E402
+from bench import ClockSampler  # noqa: E402  (nvidia-smi clocks during the timed runs)
 from paper_1010_2438_b200 import cwc  # noqa: E402
 
 SCHEDULES = {
@@ -45,6 +46,8 @@ def run(name):
     ms = a.elapsed_time(b)
     print(json.dumps(dict(config=name, schedule="one-shot", ms=round(ms, 3), firings_per_s=fir / ms * 1e3)), flush=True)
     for sch in SCHEDULES[name]:
+        clk = ClockSampler(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
+        clk.start()
         kern = [0.0]
 
         def ck(state, k):
@@ -58,10 +61,12 @@ def run(name):
             res = cwc.simulate_resumable(model, R, T, dt, 1, sweep=sweep, kernel_events=ev, checkpoint=ck, **sch)
             b.record()
             torch.cuda.synchronize()
+        clocks = clk.stop()
         same = all(torch.equal(one[k], res[k]) for k in ("count", "sum", "sumsq", "firings", "status"))
         ms = a.elapsed_time(b)
         print(json.dumps(dict(config=name, schedule=sch, ms=round(ms, 3), kernel_ms=round(kern[0], 3),
-                              advances=res["advances"], firings_per_s=fir / ms * 1e3, identical=same)), flush=True)
+                              advances=res["advances"], firings_per_s=fir / ms * 1e3, identical=same,
+                              clocks=clocks)), flush=True)
 
 
 if __name__ == "__main__":
