@@ -42,8 +42,17 @@ cwc_status cuda_fail(cudaError_t e, const char *where) {
 
 // FNV-1a over bytes (input fingerprints: staging cache, resumable-state header)
 uint64_t fnv1a(uint64_t h, const void *p, size_t n) {
+    // FNV-1a over 64-bit words, then the tail bytes (a fingerprint, not a
+    // cryptographic hash: 8x fewer steps for the staging key of big sweeps)
     const unsigned char *b = (const unsigned char *)p;
-    for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + i, 8);
+        h = (h ^ w) * 0x100000001b3ull;
+        h ^= h >> 29;
+    }
+    for (; i < n; ++i) h = (h ^ b[i]) * 0x100000001b3ull;
     return h;
 }
 template <typename T>
@@ -982,7 +991,7 @@ constexpr size_t kHdrLive = 0, kHdrCounter = 16, kHdrOut = 32, kHdrPending = 40,
 // checked by every later call on the state: layout version, the plan's
 // shape, the shard, a hash of the flat model tables and of the per-point
 // rates, and the seed (recorded by the first advance, checked by the next).
-constexpr uint64_t kPrintMagic = 0x43574352554e0003ull;  // "CWCRUN" + layout version 3
+constexpr uint64_t kPrintMagic = 0x43574352554e0004ull;  // "CWCRUN" + layout version 4
 struct RunPrint {
     uint64_t magic;
     int64_t G, J, n_cells, M, P, O, R_total, r_off;

@@ -249,9 +249,12 @@ def cwc_plan(model, n_replicas, sweep, t_end, sample_dt, opts=None):
     return info
 
 
-def cwc_simulate(model, n_replicas, sweep, t_end, sample_dt, seed, stream, stats, workspace, opts=None):
-    """stats: (count, sum, sumsq) torch tensors; workspace: uint8 torch tensor."""
-    sw = _SweepArrays(sweep) if sweep is not None else None
+def cwc_simulate(model, n_replicas, sweep, t_end, sample_dt, seed, stream, stats, workspace, opts=None,
+                 sweep_arrays=None):
+    """stats: (count, sum, sumsq) torch tensors; workspace: uint8 torch tensor;
+    sweep_arrays: a prebuilt _SweepArrays(sweep) (avoids re-marshalling a
+    large sweep on every call)."""
+    sw = sweep_arrays if sweep_arrays is not None else (_SweepArrays(sweep) if sweep is not None else None)
     st = cwc_stats(stats[0].data_ptr(), stats[1].data_ptr(), stats[2].data_ptr())
     _check(lib().cwc_simulate(model.handle, int(n_replicas), ctypes.byref(sw.c) if sw else None, float(t_end),
                               float(sample_dt), int(seed), ctypes.c_void_p(stream), st,
