@@ -307,8 +307,14 @@ def simulate_one(model, g, t_end, dt, seed, trace=None):
 
 
 def _might_overflow(rule):
+    """Whether a firing can raise a count (so the OVERFLOW rule, reading 7,
+    must look at the result): O's atoms, constructor atoms, or W / Y
+    released into the context (dissolution adds the child's counts to the
+    context's)."""
     rhs = rule["rhs"]
-    return bool(rhs.get("atoms")) or any(k.get("wrap") or k.get("content") for k in rhs.get("comps", []))
+    released = rule.get("comp") is not None and (rhs.get("release_W") or rhs.get("release_Y"))
+    return (bool(rhs.get("atoms")) or bool(released)
+            or any(k.get("wrap") or k.get("content") for k in rhs.get("comps", [])))
 
 
 def simulate(model, n_replicas, t_end, dt, seed, g_list=None):

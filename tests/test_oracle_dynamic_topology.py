@@ -215,3 +215,22 @@ def test_stoichiometry_along_a_trace():
                 assert d[4] == -1 and d[0] <= 0 and d[1] <= 0 and d[2] <= 0 and d[3] <= 0
             prev = cur
         assert len([r for r in trace if r[4] >= 0]) == fir
+
+
+@pytest.mark.parametrize("top,expect_status", [(2**31 - 2, 1), (2**31 - 1, 2)])
+def test_release_overflow_freezes_before_the_update(top, expect_status):
+    """Reading 7 (OVERFLOW) on a dissolution: releasing the child's single a
+    into a top level holding `top` of them either fits in int32 (the rule
+    fires once, then the term stalls with 2^31-1) or would not (the term
+    freezes before the update: status OVERFLOW, every sample the initial
+    state)."""
+    model = {"term": {"atoms": {"a": top}, "comps": [{"label": 1, "content": {"atoms": {"a": 1}}}]},
+             "rules": [{"label": 0, "atoms": {}, "comp": {"label": 1, "wrap": {}, "content": {}}, "rate": 1.0,
+                        "rhs": {"X": True, "release_Y": True}}],
+             "observables": [("content", 0, "a"), ("count", 1)]}
+    samples, fir, st = dyn.simulate_one(model, 0, 50.0, 10.0, 1)
+    assert st == expect_status
+    if expect_status == 1:
+        assert fir == 1 and samples[-1].tolist() == [2**31 - 1, 0]
+    else:
+        assert fir == 0 and (samples == [top, 1]).all()
