@@ -43,6 +43,18 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _deps(obj, hdrs):
+    """Headers the object was compiled against (nvcc -MD output), or every
+    header when the dependency file is missing."""
+    dfile = obj + ".d"
+    if not os.path.exists(dfile):
+        return hdrs
+    with open(dfile) as f:
+        text = f.read().replace("\\\n", " ")
+    parts = text.split(":", 1)[1].split() if ":" in text else []
+    return [d for d in parts if d.startswith(ROOT) and os.path.exists(d)] or hdrs
+
+
 def build(force=False, verbose=False):
     os.makedirs(OBJ, exist_ok=True)
     hdrs = _headers()
@@ -51,8 +63,8 @@ def build(force=False, verbose=False):
     for src in _sources():
         obj = os.path.join(OBJ, os.path.basename(src) + ".o")
         objs.append(obj)
-        if force or _stale(obj, [src] + hdrs + [__file__]):
-            jobs.append([NVCC] + FLAGS + ["-c", src, "-o", obj])
+        if force or _stale(obj, [src] + _deps(obj, hdrs) + [__file__]):
+            jobs.append([NVCC] + FLAGS + ["-MD", "-MF", obj + ".d", "-c", src, "-o", obj])
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
             futs = [ex.submit(subprocess.run, j, capture_output=True, text=True) for j in jobs]

@@ -69,6 +69,10 @@ struct DeviceBuf {
 
 }  // namespace
 
+// The calling thread's cwc_last_error() message, for the other API units
+// (dyn_api.cpp).
+void cwc::set_last_error(const std::string &msg) { g_err = msg; }
+
 struct cwc_model_s {
     // host copies
     int32_t n_species = 0, n_compartments = 0, n_cells = 0, M = 0, n_obs = 0, n_rules = 0;

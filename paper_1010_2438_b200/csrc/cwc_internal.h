@@ -2,12 +2,16 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 
 #include <cuda_runtime.h>
 
 #include "cwc.h"
 
 namespace cwc {
+
+// Sets cwc_last_error() of the calling thread (cwc_api.cpp).
+void set_last_error(const std::string &msg);
 
 // Thread path limits: cells and reactions live in registers, net change of a
 // reaction is packed as one int8 per cell into a 64-bit word.
