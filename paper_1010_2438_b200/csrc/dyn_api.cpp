@@ -197,7 +197,9 @@ cwc_status compile(const cwc_dyn_model_desc *d, cwc_dyn_model_s *m) {
                 m->dcont[(size_t)r * A + a] = m->ctor_atoms[(size_t)first * 2 * A + A + a] - lhs[2 * A + a];
             }
         }
-        m->rule[r] = make_int4(L | ((Lc + 1) << 8) | (nf << 16) | (fl << 20) | ((ns ? 0 : 1) << 24), fac[0], fac[1], 0);
+        const int single = (L == 0 && Lc < 0) ? 1 : 0;
+        m->rule[r] = make_int4(L | ((Lc + 1) << 8) | (nf << 16) | (fl << 20) | ((ns ? 0 : 1) << 24) | (single << 25),
+                               fac[0], fac[1], 0);
         m->rate[r] = d->rate[r];
         m->n_structural += ns ? 0 : 1;
     }

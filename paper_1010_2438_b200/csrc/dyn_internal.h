@@ -20,7 +20,8 @@ constexpr int kLevels = CWC_DYN_MAX_DEPTH + 1;  // depth 0 .. CWC_DYN_MAX_DEPTH
 constexpr int kSegs = 8 + 2 * CWC_DYN_MAX_CTORS;
 
 // Rule descriptor word x: label | (comp label + 1) << 8 | n factors << 16 |
-// flags (CWC_DYN_KEEP_X ...) << 20 | structural << 24.  Factors (y, z): side
+// flags (CWC_DYN_KEEP_X ...) << 20 | structural << 24 | singleton << 25
+// (a TOP rule without a child pattern: its only entry is the top level).  Factors (y, z): side
 // | atom << 4 | mult << 12 (at most two: reaction order <= 2).  w: the
 // non-structural rule's dependency mask (rules to re-evaluate after it
 // fires).
@@ -29,6 +30,7 @@ __host__ __device__ __forceinline__ int rd_comp(int x) { return ((x >> 8) & 0xff
 __host__ __device__ __forceinline__ int rd_nfac(int x) { return (x >> 16) & 0xf; }
 __host__ __device__ __forceinline__ int rd_flags(int x) { return (x >> 20) & 0xf; }
 __host__ __device__ __forceinline__ bool rd_structural(int x) { return (x >> 24) & 1; }
+__host__ __device__ __forceinline__ bool rd_singleton(int x) { return (x >> 25) & 1; }
 
 // Device tables of a compiled model (one blob per device; pointers into it).
 struct DynTables {
@@ -67,16 +69,19 @@ struct DynParams {
     unsigned long long *next_traj;
 };
 
-// Shared memory of one warp (bytes, 16-aligned): entry pairs a2 [R][32]
-// (double2), lane prefixes pre [R][32], two term buffers (wrap, content
-// [A][64] int32, label, depth [64] int8), parent / corder [64] uint8, the
-// children histogram [64] int32, rebuild segments, depth masks.
-__host__ __device__ __forceinline__ size_t dyn_a2_off() { return 0; }
-__host__ __device__ __forceinline__ size_t dyn_pre_off(int R) { return (size_t)R * 32 * 16; }
-__host__ __device__ __forceinline__ size_t dyn_term_off(int R) { return dyn_pre_off(R) + (size_t)R * 32 * 8; }
+// Shared memory of one warp (bytes, 16-aligned): the first entry of each
+// lane pair ax [R][32] (double), lane prefixes pre [R][32], the positive-entry
+// masks xm / ym [R] (bit l: entry 2l / 2l+1 > 0), two term buffers (wrap,
+// content [A][64] int32, label, depth [64] int8), then the children
+// histogram [64] int32, rebuild segments, depth masks, parent / corder [64].
+__host__ __device__ __forceinline__ size_t dyn_ax_off() { return 0; }
+__host__ __device__ __forceinline__ size_t dyn_pre_off(int R) { return (size_t)R * 32 * 8; }
+__host__ __device__ __forceinline__ size_t dyn_mask_off(int R) { return dyn_pre_off(R) + (size_t)R * 32 * 8; }
+__host__ __device__ __forceinline__ size_t dyn_term_off(int R) {
+    return (dyn_mask_off(R) + (size_t)R * 8 + 15) & ~(size_t)15;
+}
 __host__ __device__ __forceinline__ size_t dyn_term_bytes(int A) { return (size_t)2 * A * kSlots * 4 + 2 * kSlots; }
 __host__ __device__ __forceinline__ size_t dyn_misc_off(int A, int R) { return dyn_term_off(R) + 2 * dyn_term_bytes(A); }
-// misc: nchild [64] int32, seg [kSegs] int4, dmask [kLevels] u64, parent [64], corder [64]
 __host__ __device__ __forceinline__ size_t dyn_smem_per_warp(int A, int R) {
     const size_t misc = (size_t)kSlots * 4 + (size_t)kSegs * 16 + (size_t)kLevels * 8 + 2 * kSlots;
     return (dyn_misc_off(A, R) + misc + 15) & ~(size_t)15;

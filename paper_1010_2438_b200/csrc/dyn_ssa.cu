@@ -47,11 +47,18 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr long long I32MAX = 2147483647ll;
 
+// One term buffer: wrap / content [A][64] int32, label / depth [64] int8.
+struct Term {
+    int *wrap, *cont;
+    signed char *label, *depth;
+};
+
 struct Warp {
-    double2 *a2;
-    double *pre;
-    int *wrap[2], *cont[2];
-    signed char *label[2], *depth[2];
+    double *ax;             // [R][32] first entry of each lane pair
+    double *pre;            // [R][32] lane prefixes
+    unsigned *xm, *ym;      // [R] positive-entry masks of the pair's first / second entry
+    unsigned char *tbase;  // buffer b at tbase + b * tbytes (computed, never an indexed
+    unsigned tbytes, abytes;  // pointer array: that would live in local memory)
     int *nchild;
     int4 *seg;
     unsigned long long *dmask;
@@ -60,17 +67,13 @@ struct Warp {
 
 __device__ __forceinline__ Warp warp_view(unsigned char *base, int A, int R) {
     Warp w;
-    w.a2 = (double2 *)(base + dyn_a2_off());
+    w.ax = (double *)(base + dyn_ax_off());
     w.pre = (double *)(base + dyn_pre_off(R));
-    unsigned char *t = base + dyn_term_off(R);
-    const size_t tb = dyn_term_bytes(A);
-    for (int b = 0; b < 2; ++b) {
-        unsigned char *q = t + b * tb;
-        w.wrap[b] = (int *)q;
-        w.cont[b] = (int *)(q + (size_t)A * kSlots * 4);
-        w.label[b] = (signed char *)(q + (size_t)2 * A * kSlots * 4);
-        w.depth[b] = w.label[b] + kSlots;
-    }
+    w.xm = (unsigned *)(base + dyn_mask_off(R));
+    w.ym = w.xm + R;
+    w.tbase = base + dyn_term_off(R);
+    w.tbytes = (unsigned)dyn_term_bytes(A);
+    w.abytes = (unsigned)A * kSlots * 4;
     unsigned char *m = base + dyn_misc_off(A, R);
     w.nchild = (int *)m;
     w.seg = (int4 *)(m + kSlots * 4);
@@ -78,6 +81,16 @@ __device__ __forceinline__ Warp warp_view(unsigned char *base, int A, int R) {
     w.parent = m + kSlots * 4 + kSegs * 16 + kLevels * 8;
     w.corder = w.parent + kSlots;
     return w;
+}
+
+__device__ __forceinline__ Term tv(const Warp &w, int b) {
+    unsigned char *q = w.tbase + (unsigned)b * w.tbytes;
+    Term t;
+    t.wrap = (int *)q;
+    t.cont = (int *)(q + w.abytes);
+    t.label = (signed char *)(q + 2 * w.abytes);
+    t.depth = t.label + kSlots;
+    return t;
 }
 
 __device__ __forceinline__ double ks_scan(double v, int lane) {
@@ -105,8 +118,8 @@ __device__ __forceinline__ unsigned long long ballot64(bool lo, bool hi) {
 // Depth masks, parents and corder of buffer b with n slots (D1 order).
 __device__ void refresh_structure(const Warp &w, int b, int n, int lane) {
     const int s0 = lane, s1 = lane + 32;
-    const int d0 = s0 < n ? (int)w.depth[b][s0] : -1;
-    const int d1 = s1 < n ? (int)w.depth[b][s1] : -1;
+    const int d0 = s0 < n ? (int)tv(w, b).depth[s0] : -1;
+    const int d1 = s1 < n ? (int)tv(w, b).depth[s1] : -1;
 #pragma unroll
     for (int L = 0; L < kLevels; ++L) {
         const unsigned long long m = ballot64(d0 == L, d1 == L);
@@ -114,6 +127,8 @@ __device__ void refresh_structure(const Warp &w, int b, int n, int lane) {
     }
     w.nchild[s0] = 0;
     w.nchild[s1] = 0;
+    w.corder[s0] = 0;
+    w.corder[s1] = 0;
     __syncwarp();
     int par[2] = {-1, -1};
 #pragma unroll
@@ -148,14 +163,23 @@ __device__ void refresh_structure(const Warp &w, int b, int n, int lane) {
     __syncwarp();
 }
 
-// Entries of rule r at positions 2 lane, 2 lane + 1 (D1), then the rule's
-// lane prefixes; returns the rule total (all lanes).
-__device__ __forceinline__ double eval_rule(const Warp &w, const DynTables &T, int b, int n, int r, int lane) {
+// Factor of h: binomial(x, mult) for mult 1 or 2 (reaction order <= 2).
+__device__ __forceinline__ long long binom12(int x, int mult) {
+    return mult == 2 ? (((long long)x * (long long)(x - 1)) >> 1) : (long long)x;
+}
+
+// Entries of rule r at positions 2 lane, 2 lane + 1 (D1): rate k RN(h).
+__device__ __forceinline__ void rule_entries(const Warp &w, const DynTables &T, int b, int n, int r, int lane,
+                                             double &e0, double &e1) {
     const int4 d = __ldg(&T.rule[r]);
     const double k = __ldg(&T.rate[r]);
     const int L = rd_label(d.x), Lc = rd_comp(d.x), nf = rd_nfac(d.x);
-    const int *wr = w.wrap[b], *ct = w.cont[b];
-    const signed char *lab = w.label[b];
+    const Term t = tv(w, b);
+    // factor i reads row (side, atom) of the context (p) or the child (s)
+    const int f0s = d.y & 0xf, f1s = d.z & 0xf;
+    const int *row0 = (f0s == CWC_DYN_WRAP ? t.wrap : t.cont) + ((d.y >> 4) & 0xff) * kSlots;
+    const int *row1 = (f1s == CWC_DYN_WRAP ? t.wrap : t.cont) + ((d.z >> 4) & 0xff) * kSlots;
+    const int m0 = (d.y >> 12) & 0xf, m1 = (d.z >> 12) & 0xf;
     double e[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
@@ -165,40 +189,114 @@ __device__ __forceinline__ double eval_rule(const Warp &w, const DynTables &T, i
         if (Lc < 0) {
             s = pos;
             p = pos;
-            valid = pos < n && lab[pos] == L;
+            valid = pos < n && t.label[pos] == L;
         } else {
-            valid = pos < n - 1;
-            s = valid ? (int)w.corder[pos] : 0;
-            p = (int)w.parent[s];
-            valid = valid && lab[s] == Lc && lab[p] == L;
+            // positions >= n - 1 hold stale ranks: masked to a slot index
+            // (never out of the buffer) and invalidated below
+            s = (int)w.corder[pos] & (kSlots - 1);
+            p = (int)w.parent[s] & (kSlots - 1);
+            valid = pos < n - 1 && t.label[s] == Lc && t.label[p] == L;
         }
         long long h = 1;
-        for (int f = 0; f < nf; ++f) {
-            const int fac = f ? d.z : d.y;
-            const int side = fac & 0xf, atom = (fac >> 4) & 0xff, mult = (fac >> 12) & 0xf;
-            const int x = side == CWC_DYN_CTX ? ct[atom * kSlots + p]
-                                              : (side == CWC_DYN_WRAP ? wr[atom * kSlots + s] : ct[atom * kSlots + s]);
-            h *= mult == 2 ? (((long long)x * (long long)(x - 1)) >> 1) : (long long)x;
-        }
+        if (nf >= 1) h = binom12(row0[f0s == CWC_DYN_CTX ? p : s], m0);
+        if (nf >= 2) h *= binom12(row1[f1s == CWC_DYN_CTX ? p : s], m1);
         e[q] = valid ? __dmul_rn(k, __ll2double_rn(h)) : 0.0;
     }
-    const double S = ks_scan(__dadd_rn(e[0], e[1]), lane);
-    w.a2[r * 32 + lane] = make_double2(e[0], e[1]);
+    e0 = e[0];
+    e1 = e[1];
+}
+
+// The single entry (the top level) of a singleton rule, the same value in
+// every lane (broadcast loads).
+__device__ __forceinline__ double singleton_entry(const Warp &w, const DynTables &T, int b, int r) {
+    const int4 d = __ldg(&T.rule[r]);
+    const double k = __ldg(&T.rate[r]);
+    const int nf = rd_nfac(d.x);
+    const Term t = tv(w, b);
+    long long h = 1;
+    if (nf >= 1) h = binom12(t.cont[((d.y >> 4) & 0xff) * kSlots], (d.y >> 12) & 0xf);
+    if (nf >= 2) h *= binom12(t.cont[((d.z >> 4) & 0xff) * kSlots], (d.z >> 12) & 0xf);
+    return __dmul_rn(k, __ll2double_rn(h));
+}
+
+__device__ __forceinline__ void store_rule(const Warp &w, int r, int lane, double x, double y, double S) {
+    w.ax[r * 32 + lane] = x;
     w.pre[r * 32 + lane] = S;
-    return __shfl_sync(FULL, S, 31);
+    const unsigned mx = __ballot_sync(FULL, x > 0.0), my = __ballot_sync(FULL, y > 0.0);
+    if (lane == 0) {
+        w.xm[r] = mx;
+        w.ym[r] = my;
+    }
+}
+
+// Re-evaluate rules r1 and r2 (r2 < 0: none) -- entries, lane pair sums, the
+// lane prefixes (two independent shuffle scans interleaved, so two rules
+// cost one scan's latency) -- and store them; lane r receives rule r's total
+// in Tr.
+__device__ __forceinline__ void eval_rules(const Warp &w, const DynTables &T, int b, int n, int r1, int r2, int lane,
+                                           double &Tr) {
+    double a0, a1, b0 = 0.0, b1 = 0.0;
+    rule_entries(w, T, b, n, r1, lane, a0, a1);
+    if (r2 >= 0) rule_entries(w, T, b, n, r2, lane, b0, b1);
+    double u = __dadd_rn(a0, a1), v = __dadd_rn(b0, b1);
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const double yu = __shfl_up_sync(FULL, u, off);
+        const double yv = __shfl_up_sync(FULL, v, off);
+        if (lane >= off) {
+            u = __dadd_rn(u, yu);
+            v = __dadd_rn(v, yv);
+        }
+    }
+    store_rule(w, r1, lane, a0, a1, u);
+    if (r2 >= 0) store_rule(w, r2, lane, b0, b1, v);
+    const double t1 = __shfl_sync(FULL, u, 31), t2 = __shfl_sync(FULL, v, 31);
+    if (lane == r1) Tr = t1;
+    if (lane == r2) Tr = t2;
+}
+
+// Re-evaluate every rule in the mask: singletons directly (no scan: their
+// lane prefixes all equal the one entry), the others two at a time.
+__device__ __forceinline__ void eval_mask(const Warp &w, const DynTables &T, int b, int n, unsigned dirty,
+                                          unsigned single, int lane, double &Tr) {
+    unsigned sd = dirty & single;
+    dirty &= ~single;
+    while (sd) {
+        const int r = __ffs(sd) - 1;
+        sd &= sd - 1;
+        const double e = singleton_entry(w, T, b, r);
+        w.ax[r * 32 + lane] = lane == 0 ? e : 0.0;
+        w.pre[r * 32 + lane] = e;
+        if (lane == 0) {
+            w.xm[r] = e > 0.0 ? 1u : 0u;
+            w.ym[r] = 0u;
+        }
+        if (lane == r) Tr = e;
+    }
+    while (dirty) {
+        const int r1 = __ffs(dirty) - 1;
+        dirty &= dirty - 1;
+        int r2 = -1;
+        if (dirty) {
+            r2 = __ffs(dirty) - 1;
+            dirty &= dirty - 1;
+        }
+        eval_rules(w, T, b, n, r1, r2, lane, Tr);
+    }
+    __syncwarp();
 }
 
 // Observable values of buffer b (D4): lane o returns observable o.
 __device__ long long observe(const Warp &w, const DynTables &T, int b, int lane) {
     long long mine = 0;
-    const signed char *lab = w.label[b];
+    const signed char *lab = tv(w, b).label;
     const int l0 = lab[lane], l1 = lab[lane + 32];
     for (int o = 0; o < T.O; ++o) {
         unsigned long long pv = 0;
         const int k0 = __ldg(&T.obs_ptr[o]), k1 = __ldg(&T.obs_ptr[o + 1]);
         for (int k = k0; k < k1; ++k) {
             const int4 key = __ldg(&T.obs_key[k]);
-            const int *arr = key.x == CWC_DYN_OBS_WRAP ? w.wrap[b] : w.cont[b];
+            const int *arr = key.x == CWC_DYN_OBS_WRAP ? tv(w, b).wrap : tv(w, b).cont;
             if (key.x == CWC_DYN_OBS_COUNT) {
                 pv += (unsigned long long)(l0 == key.y) + (unsigned long long)(l1 == key.y);
             } else {
@@ -231,6 +329,8 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
     const Warp w = warp_view(smem + (size_t)wid * dyn_smem_per_warp(A, R), A, R);
     const StatAcc acc = stat_view(P.part, P.cells, P.st);
     const int J = P.J;
+    const unsigned all_rules = R >= 32 ? FULL : ((1u << R) - 1u);
+    const unsigned single = __ballot_sync(FULL, lane < R && rd_singleton(__ldg(&T.rule[lane < R ? lane : 0]).x)) & all_rules;
 
     for (;;) {
         long long g = 0;
@@ -245,21 +345,17 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
         for (int k = 0; k < 2; ++k) {
             const int s = lane + 32 * k;
             const bool in = s < n;
-            w.label[0][s] = in ? (signed char)__ldg(&T.init_label[s]) : (signed char)-1;
-            w.depth[0][s] = in ? (signed char)__ldg(&T.init_depth[s]) : (signed char)0;
+            tv(w, 0).label[s] = in ? (signed char)__ldg(&T.init_label[s]) : (signed char)-1;
+            tv(w, 0).depth[s] = in ? (signed char)__ldg(&T.init_depth[s]) : (signed char)0;
             for (int a = 0; a < A; ++a) {
-                w.wrap[0][a * kSlots + s] = in ? __ldg(&T.init_wrap[s * A + a]) : 0;
-                w.cont[0][a * kSlots + s] = in ? __ldg(&T.init_cont[s * A + a]) : 0;
+                tv(w, 0).wrap[a * kSlots + s] = in ? __ldg(&T.init_wrap[s * A + a]) : 0;
+                tv(w, 0).cont[a * kSlots + s] = in ? __ldg(&T.init_cont[s * A + a]) : 0;
             }
         }
         __syncwarp();
         refresh_structure(w, 0, n, lane);
         double Tr = 0.0;  // lane r: total of rule r
-        for (int r = 0; r < R; ++r) {
-            const double tot = eval_rule(w, T, 0, n, r, lane);
-            if (lane == r) Tr = tot;
-        }
-        __syncwarp();
+        eval_mask(w, T, 0, n, all_rules, single, lane, Tr);
 
         double t = 0.0;
         long long nfire = 0, firings = 0;
@@ -318,13 +414,14 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                 ls = 31 - __clz(__ballot_sync(FULL, lane == 0 ? S > 0.0 : S > Sprev));
                 fbl = true;
             }
-            const double2 pr = w.a2[rs * 32 + ls];
+            const double px = w.ax[rs * 32 + ls];
+            const bool ypos = (w.ym[rs] >> ls) & 1u, xpos = (w.xm[rs] >> ls) & 1u;
             int pos;
             if (fbl) {
-                pos = pr.y > 0.0 ? 2 * ls + 1 : 2 * ls;
+                pos = ypos ? 2 * ls + 1 : 2 * ls;
             } else {
                 const double base = __dadd_rn(Eb, ls > 0 ? w.pre[rs * 32 + ls - 1] : 0.0);
-                pos = (pr.y == 0.0 || (pr.x > 0.0 && target < __dadd_rn(base, pr.x))) ? 2 * ls : 2 * ls + 1;
+                pos = (!ypos || (xpos && target < __dadd_rn(base, px))) ? 2 * ls : 2 * ls + 1;
             }
             const int4 rd = __ldg(&T.rule[rs]);
             int p, s;
@@ -341,11 +438,11 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                 bool ovf = false;
                 long long vc = 0, vw = 0, vt = 0;
                 if (lane < A) {
-                    vc = (long long)w.cont[b][lane * kSlots + p] + __ldg(&T.dctx[rs * A + lane]);
+                    vc = (long long)tv(w, b).cont[lane * kSlots + p] + __ldg(&T.dctx[rs * A + lane]);
                     ovf = vc > I32MAX;
                     if (s >= 0) {
-                        vw = (long long)w.wrap[b][lane * kSlots + s] + __ldg(&T.dwrap[rs * A + lane]);
-                        vt = (long long)w.cont[b][lane * kSlots + s] + __ldg(&T.dcont[rs * A + lane]);
+                        vw = (long long)tv(w, b).wrap[lane * kSlots + s] + __ldg(&T.dwrap[rs * A + lane]);
+                        vt = (long long)tv(w, b).cont[lane * kSlots + s] + __ldg(&T.dcont[rs * A + lane]);
                         ovf = ovf || vw > I32MAX || vt > I32MAX;
                     }
                 }
@@ -354,10 +451,10 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                     break;
                 }
                 if (lane < A) {
-                    w.cont[b][lane * kSlots + p] = (int)vc;
+                    tv(w, b).cont[lane * kSlots + p] = (int)vc;
                     if (s >= 0) {
-                        w.wrap[b][lane * kSlots + s] = (int)vw;
-                        w.cont[b][lane * kSlots + s] = (int)vt;
+                        tv(w, b).wrap[lane * kSlots + s] = (int)vw;
+                        tv(w, b).cont[lane * kSlots + s] = (int)vt;
                     }
                 }
                 __syncwarp();
@@ -367,7 +464,7 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                 const int nb = b ^ 1;
                 const int flags = rd_flags(rd.x);
                 const bool X = flags & CWC_DYN_KEEP_X, RW = flags & CWC_DYN_RELEASE_W, RY = flags & CWC_DYN_RELEASE_Y;
-                const int dp = (int)w.depth[b][p];
+                const int dp = (int)tv(w, b).depth[p];
                 const unsigned long long live = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
                 unsigned long long le = 0;  // slots at depth <= dp
                 for (int L = 0; L <= dp; ++L) le |= w.dmask[L];
@@ -431,37 +528,37 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                         }
                         if (sg.y >= 0) {
                             const int src = sg.y + (d - sg.x);
-                            w.label[nb][d] = w.label[b][src];
-                            w.depth[nb][d] = (signed char)((int)w.depth[b][src] + sg.w);
+                            tv(w, nb).label[d] = tv(w, b).label[src];
+                            tv(w, nb).depth[d] = (signed char)((int)tv(w, b).depth[src] + sg.w);
                             for (int a = 0; a < A; ++a) {
-                                w.wrap[nb][a * kSlots + d] = w.wrap[b][a * kSlots + src];
-                                long long v = w.cont[b][a * kSlots + src];
+                                tv(w, nb).wrap[a * kSlots + d] = tv(w, b).wrap[a * kSlots + src];
+                                long long v = tv(w, b).cont[a * kSlots + src];
                                 if (src == p) {
                                     v = (X ? v - __ldg(&lhs[a]) : 0ll) + __ldg(&T.rhs[rs * A + a]);
-                                    if (RW) v += (long long)w.wrap[b][a * kSlots + s] - __ldg(&lhs[A + a]);
-                                    if (RY) v += (long long)w.cont[b][a * kSlots + s] - __ldg(&lhs[2 * A + a]);
+                                    if (RW) v += (long long)tv(w, b).wrap[a * kSlots + s] - __ldg(&lhs[A + a]);
+                                    if (RY) v += (long long)tv(w, b).cont[a * kSlots + s] - __ldg(&lhs[2 * A + a]);
                                     ovf = ovf || v > I32MAX;
                                 }
-                                w.cont[nb][a * kSlots + d] = (int)v;
+                                tv(w, nb).cont[a * kSlots + d] = (int)v;
                             }
                         } else {
                             const int c = -1 - sg.y;
                             const int4 cd = __ldg(&T.ctor[c]);
-                            w.label[nb][d] = (signed char)cd.x;
-                            w.depth[nb][d] = (signed char)(dp + 1);
+                            tv(w, nb).label[d] = (signed char)cd.x;
+                            tv(w, nb).depth[d] = (signed char)(dp + 1);
                             for (int a = 0; a < A; ++a) {
                                 long long vw = __ldg(&T.ctor_atoms[(size_t)c * 2 * A + a]);
                                 long long vc = __ldg(&T.ctor_atoms[(size_t)c * 2 * A + A + a]);
-                                if (cd.y & CWC_DYN_CTOR_W) vw += (long long)w.wrap[b][a * kSlots + s] - __ldg(&lhs[A + a]);
-                                if (cd.y & CWC_DYN_CTOR_Y) vc += (long long)w.cont[b][a * kSlots + s] - __ldg(&lhs[2 * A + a]);
+                                if (cd.y & CWC_DYN_CTOR_W) vw += (long long)tv(w, b).wrap[a * kSlots + s] - __ldg(&lhs[A + a]);
+                                if (cd.y & CWC_DYN_CTOR_Y) vc += (long long)tv(w, b).cont[a * kSlots + s] - __ldg(&lhs[2 * A + a]);
                                 ovf = ovf || vw > I32MAX || vc > I32MAX;
-                                w.wrap[nb][a * kSlots + d] = (int)vw;
-                                w.cont[nb][a * kSlots + d] = (int)vc;
+                                tv(w, nb).wrap[a * kSlots + d] = (int)vw;
+                                tv(w, nb).cont[a * kSlots + d] = (int)vc;
                             }
                         }
                     } else {
-                        w.label[nb][d] = (signed char)-1;
-                        w.depth[nb][d] = 0;
+                        tv(w, nb).label[d] = (signed char)-1;
+                        tv(w, nb).depth[d] = 0;
                     }
                 }
                 if (__any_sync(FULL, ovf)) {
@@ -472,18 +569,12 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
                 b = nb;
                 n = n_new;
                 refresh_structure(w, b, n, lane);
-                dirty = R >= 32 ? FULL : ((1u << R) - 1u);
+                dirty = all_rules;
             }
             t = tn;
             ++firings;
             // a3/a4: re-evaluate the rules the firing may have changed
-            while (dirty) {
-                const int r = __ffs(dirty) - 1;
-                dirty &= dirty - 1;
-                const double tot = eval_rule(w, T, b, n, r, lane);
-                if (lane == r) Tr = tot;
-            }
-            __syncwarp();
+            eval_mask(w, T, b, n, dirty, single, lane, Tr);
         }
         if (j <= J) {  // stall / overflow / capacity: the remaining samples take the frozen term
             const long long v = observe(w, T, b, lane);

@@ -16,6 +16,8 @@ def main():
     wpb = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     m = cwc_dyn.cwc_dyn_model_create(wd.cell_population_model())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    e1.record()  # torch creates the CUDA events on first record
     buf = None
     for it in range(4):
         r = cwc_dyn.simulate(m, n, c["t_end"], c["sample_dt"], c["seed"], kernel_events=(e0, e1), buffers=buf,
