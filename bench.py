@@ -482,12 +482,183 @@ def run_ours(args):
     return 0
 
 
+def dyn_entries(model):
+    """Match entries of the model's initial term (D1: per rule, contexts of its
+    label, times children of the pattern's label): the size of the flat
+    selection the direct method sums and searches per firing -- the
+    algorithmic-work estimate of the C6 roofline (measurement only)."""
+    comps = []  # (label, parent index)
+
+    def walk(t, label, parent):
+        me = len(comps)
+        comps.append((label, parent))
+        for c in t.get("comps", []):
+            walk(c.get("content", {}), c["label"], me)
+    walk(model["term"], 0, -1)
+    E = 0
+    for r in model["rules"]:
+        ctx = [i for i, (lab, _) in enumerate(comps) if lab == r["label"]]
+        if r.get("comp") is None:
+            E += len(ctx)
+        else:
+            E += sum(1 for (lab, par) in comps if par in ctx and lab == r["comp"]["label"])
+    return E
+
+
+def run_dyn(args):
+    """C6: the dynamic-topology path (include/cwc_dyn.h) on the cell-population
+    workload of workloads/dynamic.py; same timing rules as run_ours.  The
+    reference arm times the dynamic CPU oracle (oracle/dynamic.py)."""
+    import workloads.dynamic as wd
+    rank, world, local = _rank_env()
+    cfg = dict(wd.CONFIG_C6)
+    model_d = wd.cell_population_model()
+    block = {"workload": "C6 %s" % cfg["desc"], "points": 1, "replicas_per_point_per_gpu": cfg["n_replicas"],
+             "t_end": cfg["t_end"], "sample_dt": cfg["sample_dt"],
+             "samples": int(np.floor(cfg["t_end"] / cfg["sample_dt"])) + 1, "seed": cfg["seed"], "path": "dynamic",
+             "parallelism": "dp%d (replica shards)" % world, "l2": "flushed between timed steps (256 MiB write)"}
+
+    def oracle_dyn(g_list):
+        from oracle import dynamic as odyn
+        t0 = time.perf_counter()
+        r = odyn.simulate(model_d, 0, cfg["t_end"], cfg["sample_dt"], cfg["seed"], g_list=g_list)
+        return int(r["firings"].sum()), time.perf_counter() - t0
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        steps = []
+        for k in range(args.warmup + args.steps):
+            f, dt = oracle_dyn([k])
+            if k >= args.warmup:
+                steps.append((f, dt))
+        F, T = sum(s[0] for s in steps), sum(s[1] for s in steps)
+        sample = "1 trajectory per step of C6 (g = step index), full t_end"
+        print(json.dumps({"impl": "reference", "metric": METRIC, "value": F / T, "unit": "firings/s",
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": 1e3 * T / args.steps, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": block,
+                          "cpu_baseline": {"value": F / T, "unit": "firings/s", "cores": 1, "kind": "oracle",
+                                           "sample": sample, "cpu": _cpu_model(), "host_cores": os.cpu_count()},
+                          "e2e": {"value": F / T, "unit": "firings/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+    from paper_1010_2438_b200 import cwc_dyn
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    R = cfg["n_replicas"]
+    m = cwc_dyn.cwc_dyn_model_create(model_d)
+    ek0, ek1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ek0.record(stream)
+    ek1.record(stream)
+    kw = dict(replica_offset=rank * R, replicas_total=world * R, kernel_events=(ek0, ek1))
+    buf = None
+    for _ in range(args.warmup):
+        buf = cwc_dyn.simulate(m, R, cfg["t_end"], cfg["sample_dt"], cfg["seed"], buffers=buf, **kw)["buffers"]
+    torch.cuda.synchronize()
+    fired = int(buf["firings"].sum().item())
+    status = torch.bincount(buf["status"].long(), minlength=5).tolist()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kms = []
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    clocks = ClockSampler(vis.split(",")[local] if vis else local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        ev0[k].record(stream)
+        cwc_dyn.simulate(m, R, cfg["t_end"], cfg["sample_dt"], cfg["seed"], buffers=buf, **kw)
+        ev1[k].record(stream)
+        ev1[k].synchronize()
+        kms.append(ek0.elapsed_time(ek1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    f = torch.tensor([fired], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(f, op=dist.ReduceOp.SUM)
+    total_ms, fired_all = float(t.item()), int(f.item())
+    value = fired_all * args.steps / (total_ms / 1e3)
+    # end to end: the call plus the moments copied to pinned host memory in the timed region
+    n_cells = block["samples"] * len(model_d["observables"])
+    hc = torch.empty(4 * n_cells, dtype=torch.int64, pin_memory=True)
+    e2e_ms = []
+    for k in range(args.warmup + args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.zero_()
+        a.record(stream)
+        r = cwc_dyn.simulate(m, R, cfg["t_end"], cfg["sample_dt"], cfg["seed"], buffers=buf, **kw)
+        hc[:n_cells].copy_(r["count"].view(-1), non_blocking=True)
+        hc[n_cells:2 * n_cells].copy_(r["sum"].view(-1), non_blocking=True)
+        hc[2 * n_cells:].copy_(r["sumsq"].view(-1), non_blocking=True)
+        b.record(stream)
+        b.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    te = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = fired_all * args.steps / (float(te.item()) / 1e3)
+    props = torch.cuda.get_device_properties(dev)
+    peaks = _peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    peak_ops = props.multi_processor_count * 4 * 32 * f_max
+    E0 = dyn_entries(model_d)
+    ops = PHILOX_OPS + UNIFORM_OPS + LOG_OPS + DIV_OPS + LOOP_OPS + (E0 - 1) + E0 / 2
+    k_ms = float(np.mean(kms))
+    achieved = ops * fired / (k_ms / 1e3)
+    info = cwc_dyn.cwc_dyn_info_get(m, R, cfg["t_end"], cfg["sample_dt"])
+    line = {"metric": METRIC, "value": value, "unit": "firings/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": dict(block, kernel="dyn_ssa_kernel", capacity=info.capacity, grid=[info.blocks, info.threads],
+                           smem_per_cta=info.smem_bytes),
+            "firings_per_step": fired_all, "kernel_ms_per_step": k_ms, "status_counts": status,
+            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
+                         "frac": achieved / peak_ops, "traffic": None, "ops_per_firing": ops,
+                         "ops_model": "RNG + log + division + loop (%d) + a0 sum (E0 - 1) + search (E0 / 2) over the "
+                                      "E0 = %d match entries of the initial term: a lower bound (re-evaluated "
+                                      "entries not counted)" % (PHILOX_OPS + UNIFORM_OPS + LOG_OPS + DIV_OPS + LOOP_OPS, E0),
+                         "kernel": "dyn_ssa_kernel", "kernel_ms": k_ms,
+                         "peak_source": "issue peak = %d SMs x 4 SMSP x 32 lanes x %.0f MHz (MEASURED_PEAKS sm_max_mhz)"
+                                        % (props.multi_processor_count, f_max / 1e6)},
+            "e2e": {"value": e2e_value, "unit": "firings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 32 * n_cells},
+            "gpu_launches": 2 * args.steps, "clocks": clk}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        g_list = list(range(0, R, R // 16))[:16]
+        fo, dto = oracle_dyn(g_list)
+        line["cpu_baseline"] = {"value": fo / dto, "unit": "firings/s", "cores": 1, "kind": "oracle",
+                                "sample": "%d of %d trajectories of C6 (every %d-th g), full t_end; %.1f s (oracle/"
+                                          "dynamic.py, pure Python)" % (len(g_list), R, R // 16, dto),
+                                "cpu": _cpu_model(), "host_cores": os.cpu_count()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(wl.CONFIGS) + ["C6"],
+                    help="C1-C5: BASELINE.json configs; C6: the dynamic-topology workload (NEXT-4)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stats-mode", default="auto", choices=sorted(STATS_MODES))
@@ -499,6 +670,8 @@ def main():
         return spawn_ranks(args.gpus)
     if args.selftest_dist:
         return selftest_dist(args)
+    if args.config == "C6":
+        return run_dyn(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
