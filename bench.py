@@ -65,8 +65,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device_index):
+    def __init__(self, device_index, interval_ms=100):
         self.dev = device_index
+        self.interval_ms = int(interval_ms)
         self.proc = None
         self.path = os.path.join("/tmp", "cwc_clocks_%d_%s.csv" % (os.getpid(), device_index))
 
@@ -74,7 +75,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                                          "-lms", "100", "-i", str(self.dev)], stdout=self.f, stderr=subprocess.DEVNULL)
+                                          "-lms", str(self.interval_ms), "-i", str(self.dev)], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
@@ -369,11 +370,12 @@ def run_ours(args):
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kms, sms = [], []
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    clocks = ClockSampler(vis.split(",")[local] if vis else local)
+    clocks = ClockSampler(vis.split(",")[local] if vis else local, args.clock_ms)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    if args.clock_ms > 0:
+        clocks.start()
     for k in range(args.steps):
         flush.zero_()
         ev0[k].record(stream)
@@ -664,6 +666,8 @@ def main():
     ap.add_argument("--stats-mode", default="auto", choices=sorted(STATS_MODES))
     ap.add_argument("--dump", action="store_true", help="also write every trajectory sample to HBM (dump mode)")
     ap.add_argument("--no-all-cores", action="store_true", help="skip the all-host-cores oracle line")
+    ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling interval during the timed "
+                    "region (0: off -- for the interference A/B only)")
     ap.add_argument("--selftest-dist", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -86,8 +86,8 @@ struct cwc_model_s {
     std::vector<int4> dep_slot4;  // warp layout with the dependent's reactants inline
     std::vector<int4> dep_slot16_4;  // 16-lane segment layout with the reactants inline
     // warp kernels' per-mu tables (WarpTables.hdr / nuw / depw16 / depw32)
-    std::vector<int4> wseg_hdr, wseg_dep16, wseg_dep32;
-    std::vector<int2> wseg_nu;
+    std::vector<int4> wseg_hdr, wseg_dep16, wseg_dep32, wseg_dep4;
+    std::vector<int2> wseg_nu, wseg_nu8;
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
     int max_deps = 0;
@@ -322,6 +322,18 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
                                         m->dep_ptr[mu + 1] - m->dep_ptr[mu]);
         m->wseg_nu.resize(m->nu_cell.size());
         for (size_t q = 0; q < m->nu_cell.size(); ++q) m->wseg_nu[q] = make_int2(4 * m->nu_cell[q], m->nu_delta[q]);
+        // 4-lane groups (ssa_warp8.cu): entry m of owner ol = m / B4 at row k = m % B4
+        m->wt.B4 = std::max(1, (M + 3) / 4);
+        m->wseg_nu8.resize(m->nu_cell.size());
+        for (size_t q = 0; q < m->nu_cell.size(); ++q) m->wseg_nu8[q] = make_int2(32 * m->nu_cell[q], m->nu_delta[q]);
+        m->wseg_dep4.resize(m->dep.size());
+        for (size_t q = 0; q < m->dep.size(); ++q) {
+            const int r = m->dep[q], ol = r / m->wt.B4, k = r - ol * m->wt.B4;
+            const ReactionDesc &rd = m->rx[r];
+            const unsigned w = (unsigned)(8 * r) | ((unsigned)((ol * 4 + (k >> 4)) & 15) << 26) |
+                               ((unsigned)(rd.kind & 1) << 31);
+            m->wseg_dep4[q] = make_int4(8 * (k * 32 + (ol ^ ((k >> 2) & 3))), 32 * rd.ia, 32 * rd.ib, (int)w);
+        }
         for (int segw : {16, 32}) {
             const int Bs = segw == 16 ? m->wt.B16 : m->wt.B;
             const int Bps = Bs | 1;  // chunk stride (ssa_warp2.cu / ssa_warp.cu)
@@ -421,7 +433,8 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
                  o_dp = push_bytes(blob, m->dep_ptr), o_dep = push_bytes(blob, m->dep_slot), o_dep16 = push_bytes(blob, m->dep_slot16), o_dep4 = push_bytes(blob, m->dep_slot4), o_dep16_4 = push_bytes(blob, m->dep_slot16_4), o_op = push_bytes(blob, m->obs_ptr),
                  o_whdr = push_bytes(blob, m->wseg_hdr), o_wnu = push_bytes(blob, m->wseg_nu),
                  o_wd16 = push_bytes(blob, m->wseg_dep16), o_wd32 = push_bytes(blob, m->wseg_dep32),
-                 o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init);
+                 o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init),
+                 o_wnu8 = push_bytes(blob, m->wseg_nu8), o_wd4 = push_bytes(blob, m->wseg_dep4);
     std::unique_ptr<cwc_model_s::DevCopy> dc(new (std::nothrow) cwc_model_s::DevCopy());
     if (!dc) return fail(CWC_ERR_NOMEM, "host allocation");
     e = cudaMalloc(&dc->buf.p, blob.size());
@@ -447,6 +460,8 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
     w.nuw = (const int2 *)(b + o_wnu);
     w.depw16 = (const int4 *)(b + o_wd16);
     w.depw32 = (const int4 *)(b + o_wd32);
+    w.nuw8 = (const int2 *)(b + o_wnu8);
+    w.depw4 = (const int4 *)(b + o_wd4);
     *out = &dc->wt;
     m->dev.emplace(device, std::move(dc));
     return CWC_OK;
@@ -469,6 +484,7 @@ struct Plan {
     int stats_smem = 0;
     int ws = 0;
     int seg2 = 0;  // warp path: two trajectories per warp
+    int grp8 = 0;  // warp path: eight trajectories per warp (4-lane groups)
     int nt = 1;    // thread path, single-warp kernel: trajectories per lane
     StatLayout st{};
     int64_t cells_per_part = 0;
@@ -481,6 +497,9 @@ struct Plan {
 };
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+// the planner's automatic choice of the 4-lane-group kernel for M <= 256
+constexpr bool g_warp8_auto = false;
 
 const char *env(const char *k) {
     const char *v = std::getenv(k);
@@ -534,7 +553,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     const int smode = opts ? opts->stats_mode : CWC_STATS_AUTO;
     const int wpb = opts ? opts->warps_per_block : 0;
     const int bps = opts ? opts->blocks_per_sm : 0;
-    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_THREAD_WS2) return fail(CWC_ERR_INVALID, "bad kernel");
+    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_WARP8) return fail(CWC_ERR_INVALID, "bad kernel");
     if (smode < CWC_STATS_AUTO || smode > CWC_STATS_GLOBAL) return fail(CWC_ERR_INVALID, "bad stats_mode");
     if (wpb < 0 || wpb > 4) return fail(CWC_ERR_INVALID, "warps_per_block must be in [0, 4]");
     if (bps < 0 || bps > 32) return fail(CWC_ERR_INVALID, "blocks_per_sm must be in [0, 32]");
@@ -543,7 +562,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         kern == CWC_KERNEL_THREAD_WS2) {
         if (force == CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_THREAD;
-    } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP) {
+    } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP || kern == CWC_KERNEL_WARP8) {
         if (force == CWC_PATH_THREAD) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_WARP;
     }
@@ -665,13 +684,27 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // two trajectories per warp (16-lane segments) when a segment's chunks
         // stay short (M <= 256)
         bool seg2 = w.B16 <= 16;
+        // eight trajectories per warp (4-lane groups) for M <= 256 one-shot
+        // runs with one global statistics part (ssa_warp8.cu)
+        bool grp8 = w.B4 <= 64 && !resumable && smode != CWC_STATS_SHARED;
         if (kern == CWC_KERNEL_WARP2) {
             if (!seg2) return fail(CWC_ERR_INVALID, "kernel WARP2 needs M <= 256");
+            grp8 = false;
         } else if (kern == CWC_KERNEL_WARP) {
             seg2 = false;
+            grp8 = false;
+        } else if (kern == CWC_KERNEL_WARP8) {
+            if (!grp8) return fail(CWC_ERR_INVALID, "kernel WARP8 needs M <= 256, a one-shot run and global statistics");
+        } else if (kern == CWC_KERNEL_AUTO) {
+            grp8 = grp8 && g_warp8_auto;
         }
+        if (grp8) seg2 = false;
         pl.seg2 = seg2 ? 1 : 0;
-        const size_t per_warp = seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w);
+        pl.grp8 = grp8 ? 1 : 0;
+        if (grp8 && !wpb) W = 1;
+        pl.warps_per_block = W;
+        const size_t per_warp = grp8 ? ((warp8_smem_per_warp(w) + 15) & ~(size_t)15)
+                                     : (seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w));
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t stats = (size_t)stat_bytes(lay_s, cells);
@@ -683,7 +716,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             if (stats + W * per_warp > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
             use_smem = true;
         }
-        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable) use_smem = false;
+        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable || grp8) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
         pl.st = use_smem ? lay_s : lay_g;
         pl.cells_per_part = cells;
@@ -694,10 +727,11 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         // occupancy by shared memory / threads
         const int by_smem = (int)std::max<size_t>(1, (228 * 1024) / (pl.smem_bytes + 1024));
         const int by_threads = std::max(1, 2048 / (W * 32));
-        per_sm = std::min(by_smem, by_threads);
+        per_sm = std::min(std::min(by_smem, by_threads), 32);
         if (bps) per_sm = std::min(per_sm, bps);
         int64_t blocks = (int64_t)nsm * per_sm;
-        blocks = std::min<int64_t>(blocks, (NL + W - 1) / W);
+        const int tpw = grp8 ? 8 : (seg2 ? 2 : 1);  // trajectories per warp
+        blocks = std::min<int64_t>(blocks, (NL + (int64_t)W * tpw - 1) / ((int64_t)W * tpw));
         pl.blocks = (int)std::max<int64_t>(1, blocks);
         pl.threads = W * 32;
         // a shared-memory part takes <= 2^16 trajectories (16-bit limbs); the
@@ -812,6 +846,7 @@ cudaError_t launch_ssa(const cwc_model_s *m, const WarpTables &wt, const Plan &p
                        cudaStream_t stream) {
     if (pl.path == CWC_PATH_THREAD)
         return launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
+    if (pl.grp8) return launch_ssa_warp8(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
     return pl.seg2 ? launch_ssa_warp2(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
                    : launch_ssa_warp(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
 }
@@ -1346,7 +1381,7 @@ cwc_status cwc_plan(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, dou
     info->kernel = pl.path == CWC_PATH_THREAD
                        ? (pl.ws == 2 ? CWC_KERNEL_THREAD_WS2 : pl.ws ? CWC_KERNEL_THREAD_WS
                                                                    : (pl.nt == 2 ? CWC_KERNEL_THREAD2 : CWC_KERNEL_THREAD))
-                       : (pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
+                       : (pl.grp8 ? CWC_KERNEL_WARP8 : pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
     info->blocks = pl.path == CWC_PATH_THREAD
                        ? (pl.ws == 2 ? (int32_t)((pl.G + 63) / 64)
                                      : pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)

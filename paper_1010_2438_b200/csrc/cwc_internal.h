@@ -195,7 +195,8 @@ struct ThreadTables {
 struct WarpTables {
     int32_t n_cells, M, O, B;     // B = reactions per lane chunk = ceil(M / 32)
     int32_t Bp;                   // chunk stride (odd)
-    int32_t B16, Bp16, pad_;      // the same for 16-lane segments (ssa_warp2.cu)
+    int32_t B16, Bp16;            // the same for 16-lane segments (ssa_warp2.cu)
+    int32_t B4;                   // entries per lane of the 4-lane groups (ssa_warp8.cu): ceil(M / 4)
     const ReactionDesc *rx;       // [M]
     const int32_t *nu_ptr;        // [M+1]
     const int2 *nu;               // (cell, delta)
@@ -216,6 +217,12 @@ struct WarpTables {
     const int2 *nuw;
     const int4 *depw16;
     const int4 *depw32;
+    // 4-lane group layout (ssa_warp8.cu): net change (cell * 32, delta) and
+    // dependency entries (a byte offset (k * 32 + (owner ^ ((k >> 2) & 3))) * 8,
+    // x_a * 32, x_b * 32, m * 8 | (owner * 4 + k / 16) << 26 | sub << 31);
+    // the kernel adds its group's column / cell offsets
+    const int2 *nuw8;
+    const int4 *depw4;
 };
 
 // Launchers (ssa_thread.cu, ssa_warp.cu, stats.cu); return cudaError_t.
@@ -231,6 +238,9 @@ size_t warp_smem_per_warp(const WarpTables &wt);
 cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                              size_t smem_bytes, cudaStream_t stream);
 size_t warp2_smem_per_warp(const WarpTables &wt);
+cudaError_t launch_ssa_warp8(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+                             size_t smem_bytes, cudaStream_t stream);
+size_t warp8_smem_per_warp(const WarpTables &wt);
 
 
 cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,

@@ -89,6 +89,10 @@ def geom_for(model, kernel_variant):
         return KernelGeom(True, 32, M)
     if kernel_variant == cwc.CWC_KERNEL_WARP2:
         return KernelGeom(True, 16, M)
+    if kernel_variant == cwc.CWC_KERNEL_WARP8:
+        # 4-lane groups: sub-chunks of 16 summed left to right, four sub-chunk
+        # sums, a 4-lane shuffle tree -- within the chunk bound of B = M / 4
+        return KernelGeom(True, 4, M)
     if model.info.path == cwc.CWC_PATH_THREAD:
         return KernelGeom(False, M=M)
     return KernelGeom(True, 16 if -(-M // 16) <= 16 else 32, M)
@@ -224,7 +228,14 @@ def trace_mismatches(model, desc, sweep, cfg, g_list, warp_path=None, force_path
     from paper_1010_2438_b200 import cwc
     kern = cwc.CWC_KERNEL_AUTO if kernel is None else kernel
     fp = cwc.CWC_PATH_AUTO if force_path is None else force_path
-    geom = geom_for(model, kern)
+    # the geometry of the kernel the planner actually launches for this run
+    popts = cwc.cwc_sim_opts()
+    popts.force_path = fp
+    popts.kernel = kern
+    for k, v in plan.items():
+        setattr(popts, k, v)
+    planned = cwc.cwc_plan(model, cfg["n_replicas"], sweep, cfg["t_end"], cfg["sample_dt"], popts).kernel
+    geom = geom_for(model, planned)
     if warp_path is not None and fp != cwc.CWC_PATH_AUTO:
         geom = KernelGeom(fp == cwc.CWC_PATH_WARP, geom.lanes if geom.warp else 32, model.info.n_reactions)
     side = OracleSide(desc, sweep, cfg["n_replicas"], cfg["seed"])
