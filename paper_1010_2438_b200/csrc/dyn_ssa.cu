@@ -180,10 +180,9 @@ __device__ __forceinline__ void rule_entries(const Warp &w, const DynTables &T, 
     const int *row0 = (f0s == CWC_DYN_WRAP ? t.wrap : t.cont) + ((d.y >> 4) & 0xff) * kSlots;
     const int *row1 = (f1s == CWC_DYN_WRAP ? t.wrap : t.cont) + ((d.z >> 4) & 0xff) * kSlots;
     const int m0 = (d.y >> 12) & 0xf, m1 = (d.z >> 12) & 0xf;
-    double e[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int pos = 2 * lane + q;
+    // narrow layout (n <= 32 slots: every rule has <= 32 positions): one
+    // position per lane, pos = lane, the pair's second entry 0; wide: two
+    auto entry = [&](int pos) -> double {
         int s, p;
         bool valid;
         if (Lc < 0) {
@@ -200,10 +199,15 @@ __device__ __forceinline__ void rule_entries(const Warp &w, const DynTables &T, 
         long long h = 1;
         if (nf >= 1) h = binom12(row0[f0s == CWC_DYN_CTX ? p : s], m0);
         if (nf >= 2) h *= binom12(row1[f1s == CWC_DYN_CTX ? p : s], m1);
-        e[q] = valid ? __dmul_rn(k, __ll2double_rn(h)) : 0.0;
+        return valid ? __dmul_rn(k, __ll2double_rn(h)) : 0.0;
+    };
+    if (n <= 32) {
+        e0 = entry(lane);
+        e1 = 0.0;
+    } else {
+        e0 = entry(2 * lane);
+        e1 = entry(2 * lane + 1);
     }
-    e0 = e[0];
-    e1 = e[1];
 }
 
 // The single entry (the top level) of a singleton rule, the same value in
@@ -417,7 +421,9 @@ __global__ void __launch_bounds__(256) dyn_ssa_kernel(const DynParams P, const D
             const double px = w.ax[rs * 32 + ls];
             const bool ypos = (w.ym[rs] >> ls) & 1u, xpos = (w.xm[rs] >> ls) & 1u;
             int pos;
-            if (fbl) {
+            if (n <= 32) {  // narrow layout: position = lane
+                pos = ls;
+            } else if (fbl) {
                 pos = ypos ? 2 * ls + 1 : 2 * ls;
             } else {
                 const double base = __dadd_rn(Eb, ls > 0 ? w.pre[rs * 32 + ls - 1] : 0.0);
