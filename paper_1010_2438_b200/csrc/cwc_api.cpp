@@ -498,8 +498,12 @@ struct Plan {
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-// the planner's automatic choice of the 4-lane-group kernel for M <= 256
-constexpr bool g_warp8_auto = false;
+// the planner's automatic choice of the 4-lane-group kernel: networks of up
+// to 128 reactions (B4 <= 32).  Measured (tools/warp8_crossover.py,
+// profiles/r02/warp8/): 1.2-1.45x the two-per-warp kernel up to M = 128,
+// slower from M ~ 160 on (C4, M = 256: 3.15e9 vs 4.59e9 -- its 16 KB of
+// propensities per warp leave 9 warps per SM, too few to hide latency)
+constexpr int kWarp8AutoMaxB4 = 32;
 
 const char *env(const char *k) {
     const char *v = std::getenv(k);
@@ -696,7 +700,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         } else if (kern == CWC_KERNEL_WARP8) {
             if (!grp8) return fail(CWC_ERR_INVALID, "kernel WARP8 needs M <= 256, a one-shot run and global statistics");
         } else if (kern == CWC_KERNEL_AUTO) {
-            grp8 = grp8 && g_warp8_auto;
+            grp8 = grp8 && w.B4 <= kWarp8AutoMaxB4;
         }
         if (grp8) seg2 = false;
         pl.seg2 = seg2 ? 1 : 0;

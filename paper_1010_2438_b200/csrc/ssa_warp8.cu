@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
     const int O = wt.O, M = wt.M;
     const long long J = rp.J, J1 = J + 1;
     unsigned char *base = smem + (size_t)wib * per_warp_bytes;
-    double *aw = (double *)base;                           // [64][32]
-    double *ss = aw + 64 * 32;                             // [4][32]
+    double *aw = (double *)base;                           // [16 NS][32]
+    double *ss = aw + 16 * NS * 32;                        // [4][32]
     double2 *dr = (double2 *)(ss + 4 * 32);                // [32][8]
     int *xw = (int *)(dr + 32 * 8);                        // [n_cells + 1][8]
     const StatAcc acc = stat_view((unsigned char *)rp.parts, rp.cells_per_part, rp.st);
@@ -359,8 +359,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
     }
 }
 
-size_t warp8_smem_per_warp(const WarpTables &wt) {
-    return (size_t)8 * 64 * 32 + (size_t)8 * 4 * 32 + (size_t)16 * 32 * 8 + (size_t)4 * 8 * (wt.n_cells + 1);
+size_t warp8_smem_per_warp(const WarpTables &wt) {  // aw [16 NS][32], ss [4][32], dr [32][8], x [cells + 1][8]
+    const int NS = (wt.B4 + 15) >> 4;
+    return (size_t)8 * 16 * NS * 32 + (size_t)8 * 4 * 32 + (size_t)16 * 32 * 8 + (size_t)4 * 8 * (wt.n_cells + 1);
 }
 
 cudaError_t launch_ssa_warp8(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,

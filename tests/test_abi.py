@@ -197,13 +197,14 @@ def test_plan_override_validation():
           dict(kernel=cwc.CWC_KERNEL_WARP, warps_per_block=2, blocks_per_sm=3)]
     for kw in ok:
         assert cwc.cwc_simulate_workspace_size(c2, 64, None, 1.0, 0.1, _opts(**kw)) > 0, kw
-    bad = [(c2, dict(kernel=7)), (c2, dict(kernel=-1)), (c2, dict(stats_mode=3)), (c2, dict(warps_per_block=5)),
+    bad = [(c2, dict(kernel=8)), (c2, dict(kernel=-1)), (c2, dict(stats_mode=3)), (c2, dict(warps_per_block=5)),
            (c2, dict(warps_per_block=-1)), (c2, dict(blocks_per_sm=33)), (c2, dict(force_path=5)),
            (c2, dict(kernel=cwc.CWC_KERNEL_WARP, force_path=cwc.CWC_PATH_THREAD)),
            (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, force_path=cwc.CWC_PATH_WARP)),
            (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, block_threads=64)),
            (c5, dict(kernel=cwc.CWC_KERNEL_THREAD)),      # 264 cells: no thread path
-           (c5, dict(kernel=cwc.CWC_KERNEL_WARP2))]       # M = 1172 > 256
+           (c5, dict(kernel=cwc.CWC_KERNEL_WARP2)),       # M = 1172 > 256
+           (c5, dict(kernel=cwc.CWC_KERNEL_WARP8))]
     for m, kw in bad:
         with pytest.raises(cwc.CwcError) as ei:
             cwc.cwc_simulate_workspace_size(m, 64, None, 1.0, 0.1, _opts(**kw))
@@ -256,4 +257,25 @@ def test_plan_reports_the_kernel_and_accumulators():
         assert p.part_cells >= p.n_stat_cells if not p.stats_shared else p.part_cells > 0
     m = cwc.cwc_model_create(w.config("C2")[0])
     assert cwc.cwc_plan(m, 64, None, 1.0, 0.1, _opts(kernel=cwc.CWC_KERNEL_WARP)).kernel == cwc.CWC_KERNEL_WARP
-    assert cwc.cwc_plan(m, 64, None, 1.0, 0.1, _opts(force_path=cwc.CWC_PATH_WARP)).kernel == cwc.CWC_KERNEL_WARP2
+    assert cwc.cwc_plan(m, 64, None, 1.0, 0.1, _opts(force_path=cwc.CWC_PATH_WARP)).kernel == cwc.CWC_KERNEL_WARP8
+
+
+def test_plan_picks_the_warp_kernel_by_network_size():
+    """Planner (cwc_api.cpp): eight trajectories per warp up to 128 reactions,
+    two per warp up to 256, one per warp beyond (tools/warp8_crossover.py);
+    the 4-lane-group kernel never for resumable runs or shared-memory parts."""
+    def kern(desc, **kw):
+        o = cwc.cwc_sim_opts()
+        o.force_path = cwc.CWC_PATH_WARP
+        for k, v in kw.items():
+            setattr(o, k, v)
+        return cwc.cwc_plan(cwc.cwc_model_create(desc), 64, None, 1.0, 0.1, o).kernel
+    assert kern(w.lotka_volterra_chain(16)) == cwc.CWC_KERNEL_WARP8
+    assert kern(w.random_network_model(seed=1, n_species=64, n_reactions=128)) == cwc.CWC_KERNEL_WARP8
+    assert kern(w.random_network_model(seed=1, n_species=64, n_reactions=129)) == cwc.CWC_KERNEL_WARP2
+    assert kern(w.config("C4")[0]) == cwc.CWC_KERNEL_WARP2
+    assert kern(w.config("C5")[0]) == cwc.CWC_KERNEL_WARP
+    assert kern(w.lotka_volterra_chain(16), stats_mode=cwc.CWC_STATS_SHARED) == cwc.CWC_KERNEL_WARP2
+    assert kern(w.config("C4")[0], kernel=cwc.CWC_KERNEL_WARP8) == cwc.CWC_KERNEL_WARP8
+    with pytest.raises(cwc.CwcError):
+        kern(w.config("C5")[0], kernel=cwc.CWC_KERNEL_WARP8)

@@ -127,7 +127,8 @@ KERNELS = [("thread", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS})
            ("thread1", cwc.CWC_PATH_THREAD, {"block_threads": 64, "kernel": cwc.CWC_KERNEL_THREAD}),  # single-warp, 1/lane
            ("thread2", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD2}),  # single-warp, 2 trajectories per lane
            ("ws2", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS2}),   # warp-specialised, 2 per lane
-           ("warp", cwc.CWC_PATH_WARP, {}),                           # two trajectories per warp (M <= 256)
+           ("warp", cwc.CWC_PATH_WARP, {}),                           # the planner's warp kernel
+           ("warp2", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP2}),  # two trajectories per warp (M <= 256)
            ("warp32", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP}),  # one trajectory per warp
            ("warp8", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP8})]  # eight per warp (M <= 256)
 
@@ -140,8 +141,8 @@ def test_small_parity_full_oracle(name, make, cfg, kname, path, kw):
         pytest.skip("more than 8 cells: warp path only")
     if name in ("rnd12", "rnd24") and kname in ("thread2", "ws2"):
         pytest.skip("two trajectories per lane: M <= 8 only")
-    if name in ("cwc130", "cwc260") and kname == "warp8":
-        pytest.skip("4-lane groups: M <= 256 only")
+    if name in ("cwc130", "cwc260") and kname in ("warp8", "warp2"):
+        pytest.skip("4-lane groups / 16-lane segments: M <= 256 only")
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
     gpu = _gpu(model, cfg, sweep, want_traj=True, force_path=path, **kw)

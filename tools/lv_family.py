@@ -29,7 +29,7 @@ ap.add_argument("--t-end", type=float, default=1.0)
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 lines = []
-for n in (2, 4, 8, 16, 32):
+for n in (2, 4, 8, 16, 32, 64):
     model = cwc.cwc_model_create(wl.lotka_volterra_chain(n))
     kernels = []
     if model.info.thread_path_ok:
@@ -37,6 +37,7 @@ for n in (2, 4, 8, 16, 32):
         kernels.append(("thread", cwc.CWC_PATH_THREAD, cwc.CWC_KERNEL_THREAD))
     if (model.info.n_reactions + 15) // 16 <= 16:
         kernels.append(("warp2", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP2))
+        kernels.append(("warp8", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP8))
     kernels.append(("warp", cwc.CWC_PATH_WARP, cwc.CWC_KERNEL_WARP))
     for name, path, kern in kernels:
         clk = ClockSampler(os.environ.get("CUDA_VISIBLE_DEVICES", "0").split(",")[0])
