@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
         const double cumc = __dadd_rn(carry, sc_in);
         const unsigned hC = (__ballot_sync(kAll8, gl < NS && target < cumc) & gmask) >> gb;
         const unsigned pC = (__ballot_sync(kAll8, sv > 0.0) & gmask) >> gb;
-        const int C = hC ? __ffs(hC) - 1 : (pC ? 31 - __clz(pC) : 0);
+        // (clamped: a group without a trajectory runs this on stale shared
+        // memory, and its reads must stay inside the warp's rows)
+        const int C = min(hC ? __ffs(hC) - 1 : (pC ? 31 - __clz(pC) : 0), NS - 1);
         const double sc_ex = __shfl_up_sync(kAll8, sc_in, 1, 4);
         const double cex = __shfl_sync(kAll8, gl == 0 ? 0.0 : sc_ex, gb + C);
         const double carry2 = __dadd_rn(carry, cex);
