@@ -631,7 +631,7 @@ def run_dyn(args):
                            smem_per_cta=info.smem_bytes),
             "firings_per_step": fired_all, "kernel_ms_per_step": k_ms, "status_counts": status,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s",
-                         "frac": achieved / peak_ops, "traffic": None, "ops_per_firing": ops,
+                         "frac": achieved / peak_ops, "traffic": _ncu_traffic("C6", "dyn_ssa"), "ops_per_firing": ops,
                          "ops_model": "RNG + log + division + loop (%d) + a0 sum (E0 - 1) + search (E0 / 2) over the "
                                       "E0 = %d match entries of the initial term: a lower bound (re-evaluated "
                                       "entries not counted)" % (PHILOX_OPS + UNIFORM_OPS + LOG_OPS + DIV_OPS + LOOP_OPS, E0),

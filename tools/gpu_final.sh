@@ -10,6 +10,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 
 timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err; echo bench=$?
 for c in C1 C2 C3 C4 C5; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo $c=$?; done
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference.json 2> $OUT/bench_reference.err; echo ref=$?
+# the dynamic-topology workload (NEXT-4) and its oracle arm
+timeout 600 python bench.py --config C6 --steps 5 --warmup 3 > $OUT/bench_C6.json 2> $OUT/bench_C6.err; echo C6=$?
+timeout 300 python bench.py --config C6 --impl reference --steps 2 --warmup 1 > $OUT/bench_C6_reference.json 2> $OUT/bench_C6_reference.err; echo C6ref=$?
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_plain.json 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/launch_ncu.log 2>&1; echo launches=$?
@@ -18,10 +21,13 @@ for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do
   ncu --set full --clock-control none --import-source on -k regex:ssa_ -c 1 -o $OUT/full_$c \
       python tools/run_case.py --config $c > $OUT/ncu_$c.log 2>&1; echo full_$c=$?
 done
+python tools/dyn_probe.py 8192 > $OUT/case_C6.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:dyn_ -c 1 -o $OUT/full_C6 \
+    python tools/dyn_probe.py 8192 > $OUT/ncu_C6.log 2>&1; echo full_C6=$?
 # summaries on the box (the .ncu-rep files exceed gpurun's 64 MiB return limit):
 # counters per config, per-source-line tables, and only the default config's report
-python tools/ncu_summary.py $OUT/ncu_full_summary.json $(for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && echo $c=$OUT/full_$c.ncu-rep; done) > $OUT/ncu_summary.log 2>&1; echo summary=$?
-for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ -f $OUT/full_$c.ncu-rep ] && python tools/ncu_lines.py $OUT/full_$c.ncu-rep 60 > $OUT/lines_$c.txt 2>&1; done
+python tools/ncu_summary.py $OUT/ncu_full_summary.json $(for c in ${FULLCASES:-C2 C1 C3 C4 C5} C6; do [ -f $OUT/full_$c.ncu-rep ] && echo $c=$OUT/full_$c.ncu-rep; done) > $OUT/ncu_summary.log 2>&1; echo summary=$?
+for c in ${FULLCASES:-C2 C1 C3 C4 C5} C6; do [ -f $OUT/full_$c.ncu-rep ] && python tools/ncu_lines.py $OUT/full_$c.ncu-rep 60 > $OUT/lines_$c.txt 2>&1; done
 # dump mode: DRAM bytes of the SSA kernel with and without the trajectory dump (write amplification)
 for c in C2 C4; do
   python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} --dump > $OUT/dumpcase_$c.log 2>&1 && \
@@ -32,4 +38,4 @@ for c in C2 C4; do
       --log-file $OUT/nodump_dram_$c.csv python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} > $OUT/nodumpncu_$c.log 2>&1; echo nodump_$c=$?
 done
 mkdir -p $OUT/../reps_${TAG:-final}
-for c in ${FULLCASES:-C2 C1 C3 C4 C5}; do [ "$c" != "C2" ] && rm -f $OUT/full_$c.ncu-rep; done
+for c in ${FULLCASES:-C2 C1 C3 C4 C5} C6; do rm -f $OUT/full_$c.ncu-rep; done
