@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             unsigned dirty = 0;
 #pragma unroll 1
             for (int q = lane; q < h.w; q += 32) {
-                const int4 d = __ldg(wt.depw32 + h.z + q);
+                const int4 d = __ldcg(wt.depw32 + h.z + q);  // L2 only: the D(mu) lists stream (C5: 330 KB) and would evict the per-mu header, net-change and rate tables from L1
                 const int xa = *(const int *)((const unsigned char *)xs + d.y);
                 const int xb = *(const int *)((const unsigned char *)xs + d.z) - (int)((unsigned)d.w >> 31);
                 const double k = __ldg((const double *)((const unsigned char *)rates_h + (d.w & 0x3ffffff)));
