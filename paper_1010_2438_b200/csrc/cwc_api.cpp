@@ -938,6 +938,7 @@ cwc_status run(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, double t
     rp.J = pl.J;
     rp.dt = dt;
     rp.seed = seed;
+    set_round_keys(rp);
     rp.rates = (const double *)(w + pl.off_rates);
     rp.rates_h = rp.rates + (size_t)pl.P * std::max(m->M, 1);
     rp.n_launch = pl.G;
@@ -1142,6 +1143,7 @@ RunParams run_params(const cwc_model_s *m, const Plan &pl, const StateLayout &sl
     rp.J = pl.J;
     rp.dt = dt;
     rp.seed = seed;
+    set_round_keys(rp);
     rp.rates = (const double *)(st + sl.rates);
     rp.rates_h = rp.rates + (size_t)pl.P * std::max(m->M, 1);
     rp.parts = st + sl.parts;

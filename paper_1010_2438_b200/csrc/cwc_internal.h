@@ -118,6 +118,7 @@ struct RunParams {
     int32_t J;              // last sample index
     double dt;
     uint64_t seed;
+    uint32_t rk[20];        // Philox4x32-10 round keys of seed (round r: rk[2r], rk[2r+1]; set_round_keys)
     const double *rates;    // [P][M] flat per-reaction rate constants
     const double *rates_h;  // [P][M] the same with A + A entries halved (k / 2: segment kernel)
     // statistics: accumulator parts (see stats.cu)
@@ -163,6 +164,14 @@ struct RunParams {
     int64_t quantum;
     int64_t j_stop;
 };
+
+// Philox4x32-10 key schedule of seed: round r uses (seed_lo + r W0, seed_hi + r W1).
+inline void set_round_keys(RunParams &rp) {
+    for (int r = 0; r < 10; ++r) {
+        rp.rk[2 * r] = (uint32_t)rp.seed + (uint32_t)r * 0x9E3779B9u;
+        rp.rk[2 * r + 1] = (uint32_t)(rp.seed >> 32) + (uint32_t)r * 0xBB67AE85u;
+    }
+}
 
 __host__ __device__ __forceinline__ long long launch_traj(const RunParams &rp, long long slot) {
     return rp.rs_live ? (long long)rp.rs_live[slot] : slot;

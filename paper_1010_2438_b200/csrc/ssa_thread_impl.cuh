@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(cons
                 for (int ph = 0; ph < 4; ++ph)
                     if ((ph * B) / 4 == k) {
 #pragma unroll
-                        for (int i = 0; i < NT; ++i) pipe[i].phase(ph, rp.seed, ltab, En[i], Un[i]);
+                        for (int i = 0; i < NT; ++i) pipe[i].phase(ph, rp.rk, ltab, En[i], Un[i]);
                     }
 #pragma unroll
                 for (int i = 0; i < NT; ++i) {

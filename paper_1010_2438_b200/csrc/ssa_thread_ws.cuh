@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(32 * (1 + kWsProducers) * kWsGroups, (S * M <=
                 double Ew[PW], Uw[PW];
                 pipe.start(gk, p);
 #pragma unroll
-                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.seed, ltab, Ew, Uw);
+                for (int ph = 0; ph < 4; ++ph) pipe.phase(ph, rp.rk, ltab, Ew, Uw);
                 if (room) {
 #pragma unroll
                     for (int i = 0; i < PW; ++i) {

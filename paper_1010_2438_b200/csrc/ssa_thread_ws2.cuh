@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(32 * (1 + kWs2Producers), 1) ssa_thread_ws2_ke
 #pragma unroll
                 for (int ph = 0; ph < 4; ++ph) {
 #pragma unroll
-                    for (int q = 0; q < NS; ++q) pipe[q].phase(ph, rp.seed, ltab, Ew[q], Uw[q]);
+                    for (int q = 0; q < NS; ++q) pipe[q].phase(ph, rp.rk, ltab, Ew[q], Uw[q]);
                 }
 #pragma unroll
                 for (int q = 0; q < NS; ++q) {
