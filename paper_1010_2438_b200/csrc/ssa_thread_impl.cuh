@@ -341,7 +341,11 @@ struct ThreadBatch {
 // two warps per sub-partition raise its firings/s 1.4x).  Each trajectory's
 // batch is B / NT firings, so the draws in flight per lane stay B.
 template <int S, int M, bool TRACE, bool RES, int NT>
+#ifdef CWC_T_MAXNREG  // experiment builds: a per-thread register cap instead of the launch bounds
+__global__ void __maxnreg__(CWC_T_MAXNREG) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
+#else
 __global__ void __launch_bounds__(CWC_T_MAXT, CWC_T_MINB) ssa_thread_kernel(const RunParams rp, const ThreadTables tt) {
+#endif
     constexpr int B = (NT == 2 && ThreadBatch<M>::B >= 2) ? ThreadBatch<M>::B / 2 : ThreadBatch<M>::B;
     static_assert(NT == 1 || NT == 2, "one or two trajectories per lane");
     extern __shared__ __align__(16) unsigned char smem[];

@@ -181,3 +181,27 @@ def test_stall_and_no_rules():
     assert (r["status"].cpu().numpy() == 1).all()
     assert (r["firings"].cpu().numpy() == 0).all()
     assert (r["traj"].cpu().numpy() == np.array([1, 3, 4])).all()
+
+
+def test_cell_population_survey_scale():
+    """C6 at its bench launch shape (8192 replicas, full horizon) against the
+    oracle on the trajectories g = 0 mod 16 (512); writes the parity report
+    when CWC_PARITY_OUT names a directory."""
+    import json
+    c = wd.CONFIG_C6
+    m = cwc_dyn.cwc_dyn_model_create(wd.cell_population_model())
+    gpu = cwc_dyn.simulate(m, c["n_replicas"], c["t_end"], c["sample_dt"], c["seed"], want_traj=True)
+    torch.cuda.synchronize()
+    g_list = list(range(0, c["n_replicas"], 16))
+    traj, fir, st = oracle_runs(("cell", {}), c["t_end"], c["sample_dt"], c["seed"], g_list)
+    g_traj = gpu["traj"].cpu().numpy()[g_list]
+    same = (g_traj == traj).all(axis=(1, 2))
+    same &= gpu["firings"].cpu().numpy()[g_list] == fir
+    same &= gpu["status"].cpu().numpy()[g_list] == st
+    out = os.environ.get("CWC_PARITY_OUT")
+    if out:
+        os.makedirs(out, exist_ok=True)
+        with open(os.path.join(out, "parity_C6.json"), "w") as f:
+            json.dump({"config": "C6", "compared": len(g_list), "matched": int(same.sum()),
+                       "firings_compared": int(fir.sum()), "divergent": [int(g_list[i]) for i in np.nonzero(~same)[0]]}, f)
+    assert same.all(), ("divergent trajectories", [g_list[i] for i in np.nonzero(~same)[0]][:10])
