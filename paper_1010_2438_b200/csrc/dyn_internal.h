@@ -73,7 +73,8 @@ struct DynParams {
 // lane pair ax [R][32] (double), lane prefixes pre [R][32], the positive-entry
 // masks xm / ym [R] (bit l: entry 2l / 2l+1 > 0), two term buffers (wrap,
 // content [A][64] int32, label, depth [64] int8), then the children
-// histogram [64] int32, rebuild segments, depth masks, parent / corder [64].
+// histogram [64] int32, rebuild segments, depth masks, parent / corder [64],
+// the per-position structure words pinfo [64] (uint2).
 __host__ __device__ __forceinline__ size_t dyn_ax_off() { return 0; }
 __host__ __device__ __forceinline__ size_t dyn_pre_off(int R) { return (size_t)R * 32 * 8; }
 __host__ __device__ __forceinline__ size_t dyn_mask_off(int R) { return dyn_pre_off(R) + (size_t)R * 32 * 8; }
@@ -83,7 +84,7 @@ __host__ __device__ __forceinline__ size_t dyn_term_off(int R) {
 __host__ __device__ __forceinline__ size_t dyn_term_bytes(int A) { return (size_t)2 * A * kSlots * 4 + 2 * kSlots; }
 __host__ __device__ __forceinline__ size_t dyn_misc_off(int A, int R) { return dyn_term_off(R) + 2 * dyn_term_bytes(A); }
 __host__ __device__ __forceinline__ size_t dyn_smem_per_warp(int A, int R) {
-    const size_t misc = (size_t)kSlots * 4 + (size_t)kSegs * 16 + (size_t)kLevels * 8 + 2 * kSlots;
+    const size_t misc = (size_t)kSlots * 4 + (size_t)kSegs * 16 + (size_t)kLevels * 8 + 2 * kSlots + (size_t)kSlots * 8;
     return (dyn_misc_off(A, R) + misc + 15) & ~(size_t)15;
 }
 

@@ -63,6 +63,10 @@ struct Warp {
     int4 *seg;
     unsigned long long *dmask;
     unsigned char *parent, *corder;
+    // per entry position (rebuilt with the structure): x = label of slot pos
+    // (context rules) | label of the child at rank pos << 8 | label of its
+    // parent << 16 (0xff: no such slot / rank), y = child slot | parent << 8
+    uint2 *pinfo;
 };
 
 __device__ __forceinline__ Warp warp_view(unsigned char *base, int A, int R) {
@@ -80,6 +84,7 @@ __device__ __forceinline__ Warp warp_view(unsigned char *base, int A, int R) {
     w.dmask = (unsigned long long *)(m + kSlots * 4 + kSegs * 16);
     w.parent = m + kSlots * 4 + kSegs * 16 + kLevels * 8;
     w.corder = w.parent + kSlots;
+    w.pinfo = (uint2 *)(w.corder + kSlots);
     return w;
 }
 
@@ -161,6 +166,21 @@ __device__ void refresh_structure(const Warp &w, int b, int n, int lane) {
         }
     }
     __syncwarp();
+    const signed char *lab = tv(w, b).label;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int pos = lane + 32 * k;
+        const unsigned lctx = pos < n ? (unsigned)(unsigned char)lab[pos] : 0xffu;
+        unsigned ls = 0xffu, lp = 0xffu, sp = 0u;
+        if (pos < n - 1) {
+            const int s = w.corder[pos], p = w.parent[s];
+            ls = (unsigned)(unsigned char)lab[s];
+            lp = (unsigned)(unsigned char)lab[p];
+            sp = (unsigned)s | ((unsigned)p << 8);
+        }
+        w.pinfo[pos] = make_uint2(lctx | (ls << 8) | (lp << 16), sp);
+    }
+    __syncwarp();
 }
 
 // Factor of h: binomial(x, mult) for mult 1 or 2 (reaction order <= 2).
@@ -183,18 +203,19 @@ __device__ __forceinline__ void rule_entries(const Warp &w, const DynTables &T, 
     // narrow layout (n <= 32 slots: every rule has <= 32 positions): one
     // position per lane, pos = lane, the pair's second entry 0; wide: two
     auto entry = [&](int pos) -> double {
+        // one structure word per position (pinfo: labels and slots, 0xff
+        // labels where there is no entry)
+        const uint2 pi = w.pinfo[pos];
         int s, p;
         bool valid;
         if (Lc < 0) {
             s = pos;
             p = pos;
-            valid = pos < n && t.label[pos] == L;
+            valid = (pi.x & 0xffu) == (unsigned)L;
         } else {
-            // positions >= n - 1 hold stale ranks: masked to a slot index
-            // (never out of the buffer) and invalidated below
-            s = (int)w.corder[pos] & (kSlots - 1);
-            p = (int)w.parent[s] & (kSlots - 1);
-            valid = pos < n - 1 && t.label[s] == Lc && t.label[p] == L;
+            s = (int)(pi.y & 0xffu);
+            p = (int)((pi.y >> 8) & 0xffu);
+            valid = ((pi.x >> 8) & 0xffffu) == ((unsigned)Lc | ((unsigned)L << 8));
         }
         long long h = 1;
         if (nf >= 1) h = binom12(row0[f0s == CWC_DYN_CTX ? p : s], m0);
