@@ -60,11 +60,13 @@ enum { CWC_PATH_AUTO = -1, CWC_PATH_THREAD = 0, CWC_PATH_WARP = 1 };
    runs); THREAD_WS2: warp-specialised with two trajectories per consumer
    lane (M <= 8, one-shot runs); WARP2: two trajectories per warp (16-lane segments, M <= 256);
    WARP8: eight trajectories per warp (4-lane groups, M <= 256, one-shot runs, one global
-   statistics part); WARP: one trajectory per warp.  Every
+   statistics part); WARP4: four per warp (8-lane groups, the same conditions);
+   WARP: one trajectory per warp.  Every
    variant computes the same trajectories (up to the traced a0-sum-order
    class between the thread and warp families). */
 enum { CWC_KERNEL_AUTO = 0, CWC_KERNEL_THREAD_WS = 1, CWC_KERNEL_THREAD = 2, CWC_KERNEL_WARP2 = 3,
-       CWC_KERNEL_WARP = 4, CWC_KERNEL_THREAD2 = 5, CWC_KERNEL_THREAD_WS2 = 6, CWC_KERNEL_WARP8 = 7 };
+       CWC_KERNEL_WARP = 4, CWC_KERNEL_THREAD2 = 5, CWC_KERNEL_THREAD_WS2 = 6, CWC_KERNEL_WARP8 = 7,
+       CWC_KERNEL_WARP4 = 8 };
 
 /* Where the on-line moments accumulate (cwc_sim_opts.stats_mode): per-CTA
    shared-memory parts flushed to global memory, or one global part updated

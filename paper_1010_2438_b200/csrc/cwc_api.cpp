@@ -86,7 +86,7 @@ struct cwc_model_s {
     std::vector<int4> dep_slot4;  // warp layout with the dependent's reactants inline
     std::vector<int4> dep_slot16_4;  // 16-lane segment layout with the reactants inline
     // warp kernels' per-mu tables (WarpTables.hdr / nuw / depw16 / depw32)
-    std::vector<int4> wseg_hdr, wseg_dep16, wseg_dep32, wseg_dep4;
+    std::vector<int4> wseg_hdr, wseg_dep16, wseg_dep32, wseg_dep4, wseg_dep8;
     std::vector<int2> wseg_nu, wseg_nu8;
     std::vector<int32_t> init, obs_of_cell, obs_ptr, obs_cells;
     std::vector<ReactionDesc> rx;
@@ -334,6 +334,16 @@ cwc_status build_model(const cwc_model_desc *d, cwc_model_s *m) {
                                ((unsigned)(rd.kind & 1) << 31);
             m->wseg_dep4[q] = make_int4(8 * (k * 32 + (ol ^ ((k >> 2) & 3))), 32 * rd.ia, 32 * rd.ib, (int)w);
         }
+        // 8-lane groups: B8 = ceil(M / 8) entries per lane, two sub-chunks
+        const int B8 = std::max(1, (M + 7) / 8);
+        m->wseg_dep8.resize(m->dep.size());
+        for (size_t q = 0; q < m->dep.size(); ++q) {
+            const int r = m->dep[q], ol = r / B8, k = r - ol * B8;
+            const ReactionDesc &rd = m->rx[r];
+            const unsigned w = (unsigned)(8 * r) | ((unsigned)((ol * 2 + (k >> 4)) & 15) << 26) |
+                               ((unsigned)(rd.kind & 1) << 31);
+            m->wseg_dep8[q] = make_int4(8 * (k * 32 + (ol ^ ((k >> 1) & 7))), 32 * rd.ia, 32 * rd.ib, (int)w);
+        }
         for (int segw : {16, 32}) {
             const int Bs = segw == 16 ? m->wt.B16 : m->wt.B;
             const int Bps = Bs | 1;  // chunk stride (ssa_warp2.cu / ssa_warp.cu)
@@ -434,7 +444,8 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
                  o_whdr = push_bytes(blob, m->wseg_hdr), o_wnu = push_bytes(blob, m->wseg_nu),
                  o_wd16 = push_bytes(blob, m->wseg_dep16), o_wd32 = push_bytes(blob, m->wseg_dep32),
                  o_oc = push_bytes(blob, m->obs_cells), o_init = push_bytes(blob, m->init),
-                 o_wnu8 = push_bytes(blob, m->wseg_nu8), o_wd4 = push_bytes(blob, m->wseg_dep4);
+                 o_wnu8 = push_bytes(blob, m->wseg_nu8), o_wd4 = push_bytes(blob, m->wseg_dep4),
+                 o_wd8 = push_bytes(blob, m->wseg_dep8);
     std::unique_ptr<cwc_model_s::DevCopy> dc(new (std::nothrow) cwc_model_s::DevCopy());
     if (!dc) return fail(CWC_ERR_NOMEM, "host allocation");
     e = cudaMalloc(&dc->buf.p, blob.size());
@@ -462,6 +473,7 @@ cwc_status device_tables(cwc_model_s *m, const WarpTables **out) {
     w.depw32 = (const int4 *)(b + o_wd32);
     w.nuw8 = (const int2 *)(b + o_wnu8);
     w.depw4 = (const int4 *)(b + o_wd4);
+    w.depw8 = (const int4 *)(b + o_wd8);
     *out = &dc->wt;
     m->dev.emplace(device, std::move(dc));
     return CWC_OK;
@@ -485,6 +497,7 @@ struct Plan {
     int ws = 0;
     int seg2 = 0;  // warp path: two trajectories per warp
     int grp8 = 0;  // warp path: eight trajectories per warp (4-lane groups)
+    int grp4 = 0;  // warp path: four trajectories per warp (8-lane groups)
     int nt = 1;    // thread path, single-warp kernel: trajectories per lane
     StatLayout st{};
     int64_t cells_per_part = 0;
@@ -504,6 +517,8 @@ size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // slower from M ~ 160 on (C4, M = 256: 3.15e9 vs 4.59e9 -- its 16 KB of
 // propensities per warp leave 9 warps per SM, too few to hide latency)
 constexpr int kWarp8AutoMaxB4 = 32;
+// ... and of the 8-lane-group kernel beyond that (up to 256 reactions)
+constexpr bool kWarp4Auto = false;
 
 const char *env(const char *k) {
     const char *v = std::getenv(k);
@@ -557,7 +572,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
     const int smode = opts ? opts->stats_mode : CWC_STATS_AUTO;
     const int wpb = opts ? opts->warps_per_block : 0;
     const int bps = opts ? opts->blocks_per_sm : 0;
-    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_WARP8) return fail(CWC_ERR_INVALID, "bad kernel");
+    if (kern < CWC_KERNEL_AUTO || kern > CWC_KERNEL_WARP4) return fail(CWC_ERR_INVALID, "bad kernel");
     if (smode < CWC_STATS_AUTO || smode > CWC_STATS_GLOBAL) return fail(CWC_ERR_INVALID, "bad stats_mode");
     if (wpb < 0 || wpb > 4) return fail(CWC_ERR_INVALID, "warps_per_block must be in [0, 4]");
     if (bps < 0 || bps > 32) return fail(CWC_ERR_INVALID, "blocks_per_sm must be in [0, 32]");
@@ -566,7 +581,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         kern == CWC_KERNEL_THREAD_WS2) {
         if (force == CWC_PATH_WARP) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_THREAD;
-    } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP || kern == CWC_KERNEL_WARP8) {
+    } else if (kern == CWC_KERNEL_WARP2 || kern == CWC_KERNEL_WARP || kern == CWC_KERNEL_WARP8 || kern == CWC_KERNEL_WARP4) {
         if (force == CWC_PATH_THREAD) return fail(CWC_ERR_INVALID, "kernel does not match force_path");
         force = CWC_PATH_WARP;
     }
@@ -690,7 +705,8 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         bool seg2 = w.B16 <= 16;
         // eight trajectories per warp (4-lane groups) for M <= 256 one-shot
         // runs with one global statistics part (ssa_warp8.cu)
-        bool grp8 = w.B4 <= 64 && !resumable && smode != CWC_STATS_SHARED;
+        const bool grp_ok = w.B4 <= 64 && !resumable && smode != CWC_STATS_SHARED;
+        bool grp8 = grp_ok, grp4 = false;
         if (kern == CWC_KERNEL_WARP2) {
             if (!seg2) return fail(CWC_ERR_INVALID, "kernel WARP2 needs M <= 256");
             grp8 = false;
@@ -699,16 +715,22 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             grp8 = false;
         } else if (kern == CWC_KERNEL_WARP8) {
             if (!grp8) return fail(CWC_ERR_INVALID, "kernel WARP8 needs M <= 256, a one-shot run and global statistics");
+        } else if (kern == CWC_KERNEL_WARP4) {
+            if (!grp_ok) return fail(CWC_ERR_INVALID, "kernel WARP4 needs M <= 256, a one-shot run and global statistics");
+            grp8 = false;
+            grp4 = true;
         } else if (kern == CWC_KERNEL_AUTO) {
-            grp8 = grp8 && w.B4 <= kWarp8AutoMaxB4;
+            grp8 = grp_ok && w.B4 <= kWarp8AutoMaxB4;
+            grp4 = grp_ok && !grp8 && kWarp4Auto;
         }
-        if (grp8) seg2 = false;
+        if (grp8 || grp4) seg2 = false;
         pl.seg2 = seg2 ? 1 : 0;
         pl.grp8 = grp8 ? 1 : 0;
-        if (grp8 && !wpb) W = 1;
+        pl.grp4 = grp4 ? 1 : 0;
+        if ((grp8 || grp4) && !wpb) W = 1;
         pl.warps_per_block = W;
-        const size_t per_warp = grp8 ? ((warp8_smem_per_warp(w) + 15) & ~(size_t)15)
-                                     : (seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w));
+        const size_t per_warp = (grp8 || grp4) ? ((group_smem_per_warp(w, grp8 ? 4 : 8) + 15) & ~(size_t)15)
+                                               : (seg2 ? warp2_smem_per_warp(w) : warp_smem_per_warp(w));
         const int64_t cells = std::max<int64_t>(stat_cells_round(pl.n_stat_cells), 4);
         const StatLayout lay_s = stat_layout(true, m->vbits), lay_g = stat_layout(false, m->vbits);
         const size_t stats = (size_t)stat_bytes(lay_s, cells);
@@ -720,7 +742,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
             if (stats + W * per_warp > smem_cap) return fail(CWC_ERR_INVALID, "stats_mode SHARED: the part does not fit in shared memory");
             use_smem = true;
         }
-        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable || grp8) use_smem = false;
+        if (smode == CWC_STATS_GLOBAL || O == 0 || resumable || grp8 || grp4) use_smem = false;
         pl.stats_smem = use_smem ? 1 : 0;
         pl.st = use_smem ? lay_s : lay_g;
         pl.cells_per_part = cells;
@@ -734,7 +756,7 @@ cwc_status plan_run(const cwc_model_s *m, int64_t n_replicas, const cwc_sweep *s
         per_sm = std::min(std::min(by_smem, by_threads), 32);
         if (bps) per_sm = std::min(per_sm, bps);
         int64_t blocks = (int64_t)nsm * per_sm;
-        const int tpw = grp8 ? 8 : (seg2 ? 2 : 1);  // trajectories per warp
+        const int tpw = grp8 ? 8 : grp4 ? 4 : (seg2 ? 2 : 1);  // trajectories per warp
         blocks = std::min<int64_t>(blocks, (NL + (int64_t)W * tpw - 1) / ((int64_t)W * tpw));
         pl.blocks = (int)std::max<int64_t>(1, blocks);
         pl.threads = W * 32;
@@ -850,7 +872,8 @@ cudaError_t launch_ssa(const cwc_model_s *m, const WarpTables &wt, const Plan &p
                        cudaStream_t stream) {
     if (pl.path == CWC_PATH_THREAD)
         return launch_ssa_thread(pl.s_pad, pl.m_pad, rp, m->tt, pl.threads, pl.smem_bytes, stream);
-    if (pl.grp8) return launch_ssa_warp8(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
+    if (pl.grp8 || pl.grp4)
+        return launch_ssa_group(pl.grp8 ? 4 : 8, rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
     return pl.seg2 ? launch_ssa_warp2(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream)
                    : launch_ssa_warp(rp, wt, pl.blocks, pl.warps_per_block, pl.smem_bytes, stream);
 }
@@ -1387,7 +1410,7 @@ cwc_status cwc_plan(cwc_model m, int64_t n_replicas, const cwc_sweep *sweep, dou
     info->kernel = pl.path == CWC_PATH_THREAD
                        ? (pl.ws == 2 ? CWC_KERNEL_THREAD_WS2 : pl.ws ? CWC_KERNEL_THREAD_WS
                                                                    : (pl.nt == 2 ? CWC_KERNEL_THREAD2 : CWC_KERNEL_THREAD))
-                       : (pl.grp8 ? CWC_KERNEL_WARP8 : pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
+                       : (pl.grp8 ? CWC_KERNEL_WARP8 : pl.grp4 ? CWC_KERNEL_WARP4 : pl.seg2 ? CWC_KERNEL_WARP2 : CWC_KERNEL_WARP);
     info->blocks = pl.path == CWC_PATH_THREAD
                        ? (pl.ws == 2 ? (int32_t)((pl.G + 63) / 64)
                                      : pl.ws ? (int32_t)((pl.G + 32 * kWsGroups - 1) / (32 * kWsGroups)) : pl.blocks)

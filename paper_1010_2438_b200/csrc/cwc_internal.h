@@ -232,6 +232,7 @@ struct WarpTables {
     // the kernel adds its group's column / cell offsets
     const int2 *nuw8;
     const int4 *depw4;
+    const int4 *depw8;            // the same for 8-lane groups: (k * 32 + (owner ^ ((k >> 1) & 7))) * 8, owner * 2 + k / 16
 };
 
 // Launchers (ssa_thread.cu, ssa_warp.cu, stats.cu); return cudaError_t.
@@ -247,9 +248,10 @@ size_t warp_smem_per_warp(const WarpTables &wt);
 cudaError_t launch_ssa_warp2(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                              size_t smem_bytes, cudaStream_t stream);
 size_t warp2_smem_per_warp(const WarpTables &wt);
-cudaError_t launch_ssa_warp8(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+// LG-lane groups (ssa_warp8.cu): LG = 4 (eight trajectories per warp) or 8 (four)
+cudaError_t launch_ssa_group(int LG, const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                              size_t smem_bytes, cudaStream_t stream);
-size_t warp8_smem_per_warp(const WarpTables &wt);
+size_t group_smem_per_warp(const WarpTables &wt, int LG);
 
 
 cudaError_t launch_stats_stage2(const RunParams &rp, int64_t O, int64_t *count, int64_t *sum, uint64_t *sumsq,

@@ -1,5 +1,8 @@
-// ssa_warp8.cu -- eight trajectories per warp (4-lane groups), for the warp
-// path's medium networks (M <= 256: C4).
+// ssa_warp8.cu -- several trajectories per warp in LG-lane groups: eight
+// (LG = 4, CWC_KERNEL_WARP8) or four (LG = 8, CWC_KERNEL_WARP4), for the
+// warp path's medium networks (M <= 256).  Described below for LG = 4; with
+// LG = 8 every quantity scales (B = ceil(M/8) <= 32 entries per lane, two
+// sub-chunks, two entries per lane in the selection's read, 8-lane scans).
 //
 // Same method and result class as ssa_warp2_kernel (a0 and the selection
 // prefixes in the device's own summation tree), with
@@ -42,30 +45,39 @@ namespace {
 
 constexpr unsigned kAll8 = 0xffffffffu;
 
-// 4-lane inclusive scan (within each aligned lane quad)
-__device__ __forceinline__ double quad_scan(double v, int gl) {
-    double y = __shfl_up_sync(kAll8, v, 1, 4);
-    if (gl >= 1) v = __dadd_rn(y, v);
-    y = __shfl_up_sync(kAll8, v, 2, 4);
-    if (gl >= 2) v = __dadd_rn(y, v);
+// inclusive scan within each aligned group of LG lanes
+template <int LG>
+__device__ __forceinline__ double group_scan(double v, int gl) {
+#pragma unroll
+    for (int d = 1; d < LG; d <<= 1) {
+        const double y = __shfl_up_sync(kAll8, v, d, LG);
+        if (gl >= d) v = __dadd_rn(y, v);
+    }
     return v;
 }
 
 }  // namespace
 
-template <bool TRACE>
-__global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, const WarpTables wt, int per_warp_bytes) {
+template <int LG, bool TRACE>
+__global__ void __launch_bounds__(128) ssa_group_kernel(const RunParams rp, const WarpTables wt, int per_warp_bytes) {
+    static_assert(LG == 4 || LG == 8, "4- or 8-lane groups");
+    constexpr int TPW = 32 / LG;          // trajectories per warp
+    constexpr int EPL = 16 / LG;          // entries per lane in the selection's sub-chunk read = sub-chunks per lane
+    constexpr int SH = LG == 4 ? 2 : 1;   // log2(EPL): column swizzle (k >> SH) & (LG - 1)
+    constexpr int XSH = LG == 4 ? 0 : 1;  // x byte offsets in the tables are cell * 32 (TPW = 8)
+    constexpr unsigned GM = (1u << LG) - 1u;
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gq = lane >> 2, gl = lane & 3, gb = gq << 2;  // group, lane in group, group's first lane
-    const int B4 = wt.B4, NS = (B4 + 15) >> 4;
-    const int O = wt.O, M = wt.M;
+    const int gq = lane / LG, gl = lane & (LG - 1), gb = gq * LG;  // group, lane in group, group's first lane
+    const int M = wt.M, B4 = (M + LG - 1) / LG, NS = (B4 + 15) >> 4;
+    const int O = wt.O;
     const long long J = rp.J, J1 = J + 1;
     unsigned char *base = smem + (size_t)wib * per_warp_bytes;
     double *aw = (double *)base;                           // [16 NS][32]
     double *ss = aw + 16 * NS * 32;                        // [4][32]
-    double2 *dr = (double2 *)(ss + 4 * 32);                // [32][8]
-    int *xw = (int *)(dr + 32 * 8);                        // [n_cells + 1][8]
+    double2 *dr = (double2 *)(ss + 4 * 32);                // [32][TPW]
+    int *xw = (int *)(dr + 32 * TPW);                      // [n_cells + 1][TPW]
+    const int4 *depg = LG == 4 ? wt.depw4 : wt.depw8;
     const StatAcc acc = stat_view((unsigned char *)rp.parts, rp.cells_per_part, rp.st);
 
     bool active = false, exhausted = false;
@@ -90,9 +102,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
     };
     auto record = [&](int jj) {  // rare, divergent per group
         const long long cb = (g / rp.R) * J1 * O + (long long)jj * O;
-        for (int o = gl; o < O; o += 4) {
+        for (int o = gl; o < O; o += LG) {
             long long v = 0;
-            for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xw[__ldg(wt.obs_cells + q) * 8 + gq];
+            for (int q = __ldg(wt.obs_ptr + o); q < __ldg(wt.obs_ptr + o + 1); ++q) v += xw[__ldg(wt.obs_cells + q) * TPW + gq];
             stat_record(acc, cb + o, v);
             if (rp.out_traj) rp.out_traj[(g * J1 + jj) * O + o] = v;
         }
@@ -105,14 +117,14 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
         }
         active = false;
     };
-    // draws for ring slots [from, 32) of my group: counter nb + slot, slot = gl + 4i
+    // draws for ring slots [from, 32) of my group: counter nb + slot, slot = gl + LG i
     auto fill_draws = [&](int from, unsigned long long nb) {
 #pragma unroll 1
-        for (int sl = gl; sl < 32; sl += 4) {
+        for (int sl = gl; sl < 32; sl += LG) {
             if (sl >= from) {
                 double E, u;
                 block_to_draws(philox_block(rp.seed, gk, nb + (unsigned long long)sl), E, u);
-                dr[sl * 8 + gq] = make_double2(E, u);
+                dr[sl * TPW + gq] = make_double2(E, u);
             }
         }
     };
@@ -138,8 +150,8 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
                     for (int q = 0; q < rp.n_trace; ++q)
                         if (rp.trace_g[q] == g) tslot = q;
                 }
-                for (int c = gl; c < wt.n_cells; c += 4) xw[c * 8 + gq] = __ldg(wt.init + c);
-                if (gl == 0) xw[wt.n_cells * 8 + gq] = 1;
+                for (int c = gl; c < wt.n_cells; c += LG) xw[c * TPW + gq] = __ldg(wt.init + c);
+                if (gl == 0) xw[wt.n_cells * TPW + gq] = 1;
             }
             __syncwarp();
             if (got) {
@@ -152,9 +164,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
                     if (k < B4 && m < M) {
                         const int4 d = __ldg(reinterpret_cast<const int4 *>(wt.rx) + m);
                         a = __dmul_rn(__ldg(rates + m),
-                                      combos(xw[d.x * 8 + gq], xw[d.y * 8 + gq], d.z & 1, d.z >> 1));
+                                      combos(xw[d.x * TPW + gq], xw[d.y * TPW + gq], d.z & 1, d.z >> 1));
                     }
-                    aw[k * 32 + gb + (gl ^ ((k >> 2) & 3))] = a;
+                    aw[k * 32 + gb + (gl ^ ((k >> SH) & (LG - 1)))] = a;
                     const int c = k >> 4;
                     const double prev = (c == 0) ? sc[0] : (c == 1) ? sc[1] : (c == 2) ? sc[2] : sc[3];
                     const double nv = ((k & 15) == 0) ? a : __dadd_rn(prev, a);
@@ -165,7 +177,7 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
                 ss[1 * 32 + lane] = s1;
                 ss[2 * 32 + lane] = s2;
                 ss[3 * 32 + lane] = s3;
-                part = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
+                part = LG == 4 ? __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3) : __dadd_rn(s0, s1);
                 t = 0.0;
                 j = 0;
                 n = 0;
@@ -176,9 +188,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
                 active = true;
             }
             // group scans for everyone (groups that did not change recompute the same values)
-            const double in = quad_scan(part, gl);
-            const double a0n = __shfl_sync(kAll8, in, gb + 3);
-            const double ex = __shfl_up_sync(kAll8, in, 1, 4);
+            const double in = group_scan<LG>(part, gl);
+            const double a0n = __shfl_sync(kAll8, in, gb + LG - 1);
+            const double ex = __shfl_up_sync(kAll8, in, 1, LG);
             if (got) {
                 incl = in;
                 a0 = a0n;
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
             if (active) fill_draws(0, n);
             __syncwarp();
         }
-        const double2 d2 = dr[slot * 8 + gq];
+        const double2 d2 = dr[slot * TPW + gq];
         const double E = d2.x, u2 = d2.y;
         const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
         const double tn = __dadd_rn(t, tau);
@@ -225,43 +237,46 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
 
         // ---- selection (a8) ----
         const double target = __dmul_rn(u2, a0);
-        const unsigned gmask = 0xfu << gb;
+        const unsigned gmask = GM << gb;
         const unsigned hL = (__ballot_sync(kAll8, incl > target) & gmask) >> gb;
         const unsigned pL = (__ballot_sync(kAll8, part > 0.0) & gmask) >> gb;
         const int L = hL ? __ffs(hL) - 1 : (pL ? 31 - __clz(pL) : 0);
         const double carry = __shfl_sync(kAll8, excl, gb + L);
         // owner L's sub-chunk sums: lane gl takes sub-chunk gl
-        const double sv = ss[gl * 32 + gb + L];
-        const double sc_in = quad_scan(sv, gl);
+        const double sv = gl < NS ? ss[gl * 32 + gb + L] : 0.0;
+        const double sc_in = group_scan<LG>(sv, gl);
         const double cumc = __dadd_rn(carry, sc_in);
         const unsigned hC = (__ballot_sync(kAll8, gl < NS && target < cumc) & gmask) >> gb;
         const unsigned pC = (__ballot_sync(kAll8, sv > 0.0) & gmask) >> gb;
         // (clamped: a group without a trajectory runs this on stale shared
         // memory, and its reads must stay inside the warp's rows)
         const int C = min(hC ? __ffs(hC) - 1 : (pC ? 31 - __clz(pC) : 0), NS - 1);
-        const double sc_ex = __shfl_up_sync(kAll8, sc_in, 1, 4);
+        const double sc_ex = __shfl_up_sync(kAll8, sc_in, 1, LG);
         const double cex = __shfl_sync(kAll8, gl == 0 ? 0.0 : sc_ex, gb + C);
         const double carry2 = __dadd_rn(carry, cex);
-        // four consecutive entries of sub-chunk C of owner L per lane
-        const int k0 = 16 * C + 4 * gl;
-        const int col = gb + (L ^ gl);  // (k >> 2) & 3 == gl for k in [k0, k0 + 4)
-        const double e0 = aw[(k0 + 0) * 32 + col], e1 = aw[(k0 + 1) * 32 + col];
-        const double e2 = aw[(k0 + 2) * 32 + col], e3 = aw[(k0 + 3) * 32 + col];
-        const double l1 = __dadd_rn(e0, e1), l2 = __dadd_rn(l1, e2), l3 = __dadd_rn(l2, e3);
-        const double lin = quad_scan(l3, gl);
-        const double lex = __shfl_up_sync(kAll8, lin, 1, 4);
+        // EPL consecutive entries of sub-chunk C of owner L per lane
+        const int k0 = 16 * C + EPL * gl;
+        const int col = gb + (L ^ gl);  // (k >> SH) & (LG - 1) == gl for k in [k0, k0 + EPL)
+        double ev[EPL], lp[EPL];
+#pragma unroll
+        for (int i = 0; i < EPL; ++i) {
+            ev[i] = aw[(k0 + i) * 32 + col];
+            lp[i] = i ? __dadd_rn(lp[i - 1], ev[i]) : ev[i];
+        }
+        const double lin = group_scan<LG>(lp[EPL - 1], gl);
+        const double lex = __shfl_up_sync(kAll8, lin, 1, LG);
         const double b0 = __dadd_rn(carry2, gl == 0 ? 0.0 : lex);
-        int hi_ = -1;
-        if (target < __dadd_rn(b0, e0)) hi_ = 0;
-        else if (target < __dadd_rn(b0, l1)) hi_ = 1;
-        else if (target < __dadd_rn(b0, l2)) hi_ = 2;
-        else if (target < __dadd_rn(b0, l3)) hi_ = 3;
-        const int lastpos = e3 > 0.0 ? 3 : e2 > 0.0 ? 2 : e1 > 0.0 ? 1 : e0 > 0.0 ? 0 : -1;
+        int hi_ = -1, lastpos = -1;
+#pragma unroll
+        for (int i = EPL - 1; i >= 0; --i) {
+            if (target < __dadd_rn(b0, lp[i])) hi_ = i;
+            if (lastpos < 0 && ev[i] > 0.0) lastpos = i;
+        }
         const unsigned hE = (__ballot_sync(kAll8, hi_ >= 0) & gmask) >> gb;
         const unsigned pE = (__ballot_sync(kAll8, lastpos >= 0) & gmask) >> gb;
         const int G = hE ? __ffs(hE) - 1 : (pE ? 31 - __clz(pE) : 0);
         const int iG = __shfl_sync(kAll8, hE ? hi_ : lastpos, gb + G);
-        const int mu = L * B4 + 16 * C + 4 * G + (iG < 0 ? 0 : iG);
+        const int mu = L * B4 + 16 * C + EPL * G + (iG < 0 ? 0 : iG);
         if (TRACE && fire) trace_rec(n, a0, tau, tn, mu);
 
         // ---- update (a9): one lane per changed cell ----
@@ -270,11 +285,11 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
         long long nv = 0;
         if (gl < h.y) {  // |nu| <= 4 for order <= 2 reactions with <= 2 products
             e = __ldg(wt.nuw8 + h.x + gl);  // (cell * 32, delta)
-            nv = (long long)*(const int *)((const unsigned char *)xw + e.x + gq * 4) + e.y;
+            nv = (long long)*(const int *)((const unsigned char *)xw + (e.x >> XSH) + gq * 4) + e.y;
         }
-        for (int q = gl + 4; q < h.y; q += 4) {  // (more than four changed cells)
+        for (int q = gl + LG; q < h.y; q += LG) {  // (more than LG changed cells)
             const int2 e2 = __ldg(wt.nuw8 + h.x + q);
-            const long long v2 = (long long)*(const int *)((const unsigned char *)xw + e2.x + gq * 4) + e2.y;
+            const long long v2 = (long long)*(const int *)((const unsigned char *)xw + (e2.x >> XSH) + gq * 4) + e2.y;
             nv = v2 > nv ? v2 : nv;  // only the overflow test needs it here
         }
         const bool ovf = ((__ballot_sync(kAll8, nv > 0x7fffffffll) & gmask) != 0u);
@@ -287,9 +302,9 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
             __syncwarp();
         }
         if (fire) {
-            for (int q = gl; q < h.y; q += 4) {
+            for (int q = gl; q < h.y; q += LG) {
                 const int2 e2 = __ldg(wt.nuw8 + h.x + q);
-                int *px = (int *)((unsigned char *)xw + e2.x + gq * 4);
+                int *px = (int *)((unsigned char *)xw + (e2.x >> XSH) + gq * 4);
                 *px = *px + e2.y;
             }
         }
@@ -302,13 +317,13 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
         unsigned dirty = 0;
         if (fire) {
 #pragma unroll 1
-            for (int q0 = 0; q0 < h.w; q0 += 16) {
+            for (int q0 = 0; q0 < h.w; q0 += 4 * LG) {
                 int4 dd[4];
                 double kk[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int q = q0 + gl + 4 * i;
-                    dd[i] = q < h.w ? __ldg(wt.depw4 + h.z + q) : make_int4(0, 0, 0, -1);
+                    const int q = q0 + gl + LG * i;
+                    dd[i] = q < h.w ? __ldg(depg + h.z + q) : make_int4(0, 0, 0, -1);
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -317,17 +332,17 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
                 for (int i = 0; i < 4; ++i) {
                     if (dd[i].w == -1) continue;
                     const int4 d = dd[i];
-                    const int xa = *(const int *)((const unsigned char *)xw + d.y + gq * 4);
-                    const int xb = *(const int *)((const unsigned char *)xw + d.z + gq * 4) - (int)((unsigned)d.w >> 31);
+                    const int xa = *(const int *)((const unsigned char *)xw + (d.y >> XSH) + gq * 4);
+                    const int xb = *(const int *)((const unsigned char *)xw + (d.z >> XSH) + gq * 4) - (int)((unsigned)d.w >> 31);
                     *(double *)((unsigned char *)aw + d.x + gb * 8) =
                         __dmul_rn(kk[i], __dmul_rn(__int2double_rn(xa), __int2double_rn(xb)));
                     dirty |= 1u << (((unsigned)d.w >> 26) & 15u);
                 }
             }
         }
-        dirty |= __shfl_xor_sync(kAll8, dirty, 1);
-        dirty |= __shfl_xor_sync(kAll8, dirty, 2);
-        const unsigned mine = (dirty >> (4 * gl)) & 0xfu;
+#pragma unroll
+        for (int d = 1; d < LG; d <<= 1) dirty |= __shfl_xor_sync(kAll8, dirty, d);
+        const unsigned mine = (dirty >> (EPL * gl)) & ((1u << EPL) - 1u);
         __syncwarp();
         // ---- dirty sub-chunks re-summed by their owners: the four sums as
         // independent chains in one pass (predicated per sub-chunk) ----
@@ -336,21 +351,21 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-                const int cofs = gb + (gl ^ ((i >> 2) & 3));
+                const int cofs = gb + (gl ^ ((i >> SH) & (LG - 1)));
                 if (r0) { const double a = aw[i * 32 + cofs]; t0 = i ? __dadd_rn(t0, a) : a; }
                 if (r1) { const double a = aw[(16 + i) * 32 + cofs]; t1 = i ? __dadd_rn(t1, a) : a; }
-                if (r2) { const double a = aw[(32 + i) * 32 + cofs]; t2 = i ? __dadd_rn(t2, a) : a; }
-                if (r3) { const double a = aw[(48 + i) * 32 + cofs]; t3 = i ? __dadd_rn(t3, a) : a; }
+                if (LG == 4 && r2) { const double a = aw[(32 + i) * 32 + cofs]; t2 = i ? __dadd_rn(t2, a) : a; }
+                if (LG == 4 && r3) { const double a = aw[(48 + i) * 32 + cofs]; t3 = i ? __dadd_rn(t3, a) : a; }
             }
             if (r0) { s0 = t0; ss[0 * 32 + lane] = s0; }
             if (r1) { s1 = t1; ss[1 * 32 + lane] = s1; }
-            if (r2) { s2 = t2; ss[2 * 32 + lane] = s2; }
-            if (r3) { s3 = t3; ss[3 * 32 + lane] = s3; }
+            if (LG == 4 && r2) { s2 = t2; ss[2 * 32 + lane] = s2; }
+            if (LG == 4 && r3) { s3 = t3; ss[3 * 32 + lane] = s3; }
         }
-        if (mine) part = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3);
-        incl = quad_scan(part, gl);
-        a0 = __shfl_sync(kAll8, incl, gb + 3);
-        excl = __shfl_up_sync(kAll8, incl, 1, 4);
+        if (mine) part = LG == 4 ? __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), s2), s3) : __dadd_rn(s0, s1);
+        incl = group_scan<LG>(part, gl);
+        a0 = __shfl_sync(kAll8, incl, gb + LG - 1);
+        excl = __shfl_up_sync(kAll8, incl, 1, LG);
         if (gl == 0) excl = 0.0;
         if (fire) {  // (an active group that did not fire has finished)
             t = tn;
@@ -361,15 +376,16 @@ __global__ void __launch_bounds__(128) ssa_warp8_kernel(const RunParams rp, cons
     }
 }
 
-size_t warp8_smem_per_warp(const WarpTables &wt) {  // aw [16 NS][32], ss [4][32], dr [32][8], x [cells + 1][8]
-    const int NS = (wt.B4 + 15) >> 4;
-    return (size_t)8 * 16 * NS * 32 + (size_t)8 * 4 * 32 + (size_t)16 * 32 * 8 + (size_t)4 * 8 * (wt.n_cells + 1);
+size_t group_smem_per_warp(const WarpTables &wt, int LG) {  // aw [16 NS][32], ss [4][32], dr [32][TPW], x [cells + 1][TPW]
+    const int B = (wt.M + LG - 1) / LG, NS = (B + 15) >> 4, TPW = 32 / LG;
+    return (size_t)8 * 16 * NS * 32 + (size_t)8 * 4 * 32 + (size_t)16 * 32 * TPW + (size_t)4 * TPW * (wt.n_cells + 1);
 }
 
-cudaError_t launch_ssa_warp8(const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
+cudaError_t launch_ssa_group(int LG, const RunParams &rp, const WarpTables &wt, int blocks, int warps_per_block,
                              size_t smem_bytes, cudaStream_t stream) {
-    const int per_warp = (int)((warp8_smem_per_warp(wt) + 15) & ~(size_t)15);
-    auto k = rp.n_trace > 0 ? ssa_warp8_kernel<true> : ssa_warp8_kernel<false>;
+    const int per_warp = (int)((group_smem_per_warp(wt, LG) + 15) & ~(size_t)15);
+    auto k = LG == 4 ? (rp.n_trace > 0 ? ssa_group_kernel<4, true> : ssa_group_kernel<4, false>)
+                     : (rp.n_trace > 0 ? ssa_group_kernel<8, true> : ssa_group_kernel<8, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<blocks, warps_per_block * 32, smem_bytes, stream>>>(rp, wt, per_warp);

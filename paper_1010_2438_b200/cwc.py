@@ -22,7 +22,7 @@ CWC_OK, CWC_ERR_INVALID, CWC_ERR_UNSUPPORTED, CWC_ERR_CUDA, CWC_ERR_NOMEM = 0, -
 CWC_TRAJ_DONE, CWC_TRAJ_STALLED, CWC_TRAJ_OVERFLOW, CWC_TRAJ_RUNNING = 0, 1, 2, 3
 CWC_PATH_AUTO, CWC_PATH_THREAD, CWC_PATH_WARP = -1, 0, 1
 CWC_KERNEL_AUTO, CWC_KERNEL_THREAD_WS, CWC_KERNEL_THREAD, CWC_KERNEL_WARP2, CWC_KERNEL_WARP, CWC_KERNEL_THREAD2, \
-    CWC_KERNEL_THREAD_WS2, CWC_KERNEL_WARP8 = 0, 1, 2, 3, 4, 5, 6, 7
+    CWC_KERNEL_THREAD_WS2, CWC_KERNEL_WARP8, CWC_KERNEL_WARP4 = 0, 1, 2, 3, 4, 5, 6, 7, 8
 CWC_STATS_AUTO, CWC_STATS_SHARED, CWC_STATS_GLOBAL = 0, 1, 2
 
 EXPORTED = ["cwc_plan", "cwc_model_create", "cwc_model_destroy", "cwc_model_info_get", "cwc_model_get_flat",
@@ -238,7 +238,7 @@ def cwc_simulate_workspace_size(model, n_replicas, sweep, t_end, sample_dt, opts
 KERNEL_NAMES = {CWC_KERNEL_THREAD_WS: "ssa_thread_ws_kernel", CWC_KERNEL_THREAD: "ssa_thread_kernel",
                 CWC_KERNEL_THREAD2: "ssa_thread_kernel", CWC_KERNEL_THREAD_WS2: "ssa_thread_ws2_kernel",
                 CWC_KERNEL_WARP2: "ssa_warp2_kernel", CWC_KERNEL_WARP: "ssa_warp_kernel",
-                CWC_KERNEL_WARP8: "ssa_warp8_kernel"}
+                CWC_KERNEL_WARP8: "ssa_group_kernel<4", CWC_KERNEL_WARP4: "ssa_group_kernel<8"}
 
 
 def cwc_plan(model, n_replicas, sweep, t_end, sample_dt, opts=None):

@@ -197,14 +197,14 @@ def test_plan_override_validation():
           dict(kernel=cwc.CWC_KERNEL_WARP, warps_per_block=2, blocks_per_sm=3)]
     for kw in ok:
         assert cwc.cwc_simulate_workspace_size(c2, 64, None, 1.0, 0.1, _opts(**kw)) > 0, kw
-    bad = [(c2, dict(kernel=8)), (c2, dict(kernel=-1)), (c2, dict(stats_mode=3)), (c2, dict(warps_per_block=5)),
+    bad = [(c2, dict(kernel=9)), (c2, dict(kernel=-1)), (c2, dict(stats_mode=3)), (c2, dict(warps_per_block=5)),
            (c2, dict(warps_per_block=-1)), (c2, dict(blocks_per_sm=33)), (c2, dict(force_path=5)),
            (c2, dict(kernel=cwc.CWC_KERNEL_WARP, force_path=cwc.CWC_PATH_THREAD)),
            (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, force_path=cwc.CWC_PATH_WARP)),
            (c2, dict(kernel=cwc.CWC_KERNEL_THREAD_WS, block_threads=64)),
            (c5, dict(kernel=cwc.CWC_KERNEL_THREAD)),      # 264 cells: no thread path
            (c5, dict(kernel=cwc.CWC_KERNEL_WARP2)),       # M = 1172 > 256
-           (c5, dict(kernel=cwc.CWC_KERNEL_WARP8))]
+           (c5, dict(kernel=cwc.CWC_KERNEL_WARP8)), (c5, dict(kernel=cwc.CWC_KERNEL_WARP4))]
     for m, kw in bad:
         with pytest.raises(cwc.CwcError) as ei:
             cwc.cwc_simulate_workspace_size(m, 64, None, 1.0, 0.1, _opts(**kw))

@@ -130,7 +130,8 @@ KERNELS = [("thread", cwc.CWC_PATH_THREAD, {"kernel": cwc.CWC_KERNEL_THREAD_WS})
            ("warp", cwc.CWC_PATH_WARP, {}),                           # the planner's warp kernel
            ("warp2", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP2}),  # two trajectories per warp (M <= 256)
            ("warp32", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP}),  # one trajectory per warp
-           ("warp8", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP8})]  # eight per warp (M <= 256)
+           ("warp8", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP8}),  # eight per warp (M <= 256)
+           ("warp4", cwc.CWC_PATH_WARP, {"kernel": cwc.CWC_KERNEL_WARP4})]  # four per warp (M <= 256)
 
 
 @pytest.mark.parametrize("name,make,cfg", SMALL, ids=[s[0] for s in SMALL])
@@ -141,7 +142,7 @@ def test_small_parity_full_oracle(name, make, cfg, kname, path, kw):
         pytest.skip("more than 8 cells: warp path only")
     if name in ("rnd12", "rnd24") and kname in ("thread2", "ws2"):
         pytest.skip("two trajectories per lane: M <= 8 only")
-    if name in ("cwc130", "cwc260") and kname in ("warp8", "warp2"):
+    if name in ("cwc130", "cwc260") and kname in ("warp8", "warp4", "warp2"):
         pytest.skip("4-lane groups / 16-lane segments: M <= 256 only")
     desc, sweep = make()
     model = cwc.cwc_model_create(desc)
@@ -217,7 +218,8 @@ def test_finalize_matches_oracle_moments():
         assert np.all(np.abs(g - wv) <= 1e-9 * np.maximum(np.abs(g), np.abs(wv)))
 
 
-@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_WARP2, cwc.CWC_KERNEL_WARP, cwc.CWC_KERNEL_WARP8])
+@pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_WARP2, cwc.CWC_KERNEL_WARP, cwc.CWC_KERNEL_WARP8,
+                                  cwc.CWC_KERNEL_WARP4])
 def test_trace_warp_paths_against_oracle(kern):
     """The warp kernels' per-firing traces (n, a0, tau, t', mu) against the
     oracle's: identical or differing only by the classified ulp-level

@@ -89,6 +89,8 @@ def geom_for(model, kernel_variant):
         return KernelGeom(True, 32, M)
     if kernel_variant == cwc.CWC_KERNEL_WARP2:
         return KernelGeom(True, 16, M)
+    if kernel_variant == cwc.CWC_KERNEL_WARP4:
+        return KernelGeom(True, 8, M)  # 8-lane groups (same construction, B = M / 8)
     if kernel_variant == cwc.CWC_KERNEL_WARP8:
         # 4-lane groups: sub-chunks of 16 summed left to right, four sub-chunk
         # sums, a 4-lane shuffle tree -- within the chunk bound of B = M / 4

@@ -30,7 +30,7 @@ if a.lib:
     cwc.LIB_PATH = os.path.abspath(a.lib)
 K = {"auto": cwc.CWC_KERNEL_AUTO, "ws": cwc.CWC_KERNEL_THREAD_WS, "single": cwc.CWC_KERNEL_THREAD,
      "warp2": cwc.CWC_KERNEL_WARP2, "warp": cwc.CWC_KERNEL_WARP, "thread2": cwc.CWC_KERNEL_THREAD2,
-     "ws2": cwc.CWC_KERNEL_THREAD_WS2, "warp8": cwc.CWC_KERNEL_WARP8}[a.kernel]
+     "ws2": cwc.CWC_KERNEL_THREAD_WS2, "warp8": cwc.CWC_KERNEL_WARP8, "warp4": cwc.CWC_KERNEL_WARP4}[a.kernel]
 desc, sweep, cfg = w.config(a.config)
 if a.t_end:
     cfg["t_end"] = a.t_end

@@ -1,4 +1,4 @@
-"""Two- vs eight-trajectories-per-warp kernels across network sizes (the
+"""Two- vs four- vs eight-trajectories-per-warp kernels across network sizes (the
 planner's crossover): random networks (workloads.random_network_model, the C4
 generator at other sizes) and n-species Lotka-Volterra chains; firings/s by
 kernel events, best of 3, with nvidia-smi clocks."""
@@ -21,7 +21,7 @@ ev[1].record()
 for name, M, make in cases:
     model = cwc.cwc_model_create(make())
     t_end = 0.2 if name == "rnd" else 0.2
-    for kname, kern in (("warp2", cwc.CWC_KERNEL_WARP2), ("warp8", cwc.CWC_KERNEL_WARP8)):
+    for kname, kern in (("warp2", cwc.CWC_KERNEL_WARP2), ("warp8", cwc.CWC_KERNEL_WARP8), ("warp4", cwc.CWC_KERNEL_WARP4)):
         buf, best = None, None
         clk = ClockSampler(0)
         clk.start()
