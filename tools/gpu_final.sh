@@ -28,6 +28,12 @@ ncu --set full --clock-control none --import-source on -k regex:dyn_ -c 1 -o $OU
 # counters per config, per-source-line tables, and only the default config's report
 python tools/ncu_summary.py $OUT/ncu_full_summary.json $(for c in ${FULLCASES:-C2 C1 C3 C4 C5} C6; do [ -f $OUT/full_$c.ncu-rep ] && echo $c=$OUT/full_$c.ncu-rep; done) > $OUT/ncu_summary.log 2>&1; echo summary=$?
 for c in ${FULLCASES:-C2 C1 C3 C4 C5} C6; do [ -f $OUT/full_$c.ncu-rep ] && python tools/ncu_lines.py $OUT/full_$c.ncu-rep 60 > $OUT/lines_$c.txt 2>&1; done
+# parity reports (survey subsets, every trajectory of the five configs, C6)
+if [ -n "$PARITY" ]; then
+  CWC_PARITY_OUT=$OUT/parity_scale timeout 1200 python -m pytest tests/test_gpu_parity_scale.py -q > $OUT/parity_scale.log 2>&1; echo parity_scale=$?
+  CWC_PARITY_FULL=1 CWC_PARITY_OUT=$OUT/parity_full timeout 2400 python -m pytest tests/test_gpu_parity_full.py -q > $OUT/parity_full.log 2>&1; echo parity_full=$?
+  CWC_PARITY_OUT=$OUT/parity_dyn timeout 900 python -m pytest tests/test_gpu_dynamic.py -q -k survey > $OUT/parity_dyn.log 2>&1; echo parity_dyn=$?
+fi
 # dump mode: DRAM bytes of the SSA kernel with and without the trajectory dump (write amplification)
 for c in C2 C4; do
   python tools/run_case.py --config $c --t-end ${DUMP_T:-0.5} --dump > $OUT/dumpcase_$c.log 2>&1 && \
