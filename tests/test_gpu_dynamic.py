@@ -205,3 +205,36 @@ def test_cell_population_survey_scale():
             json.dump({"config": "C6", "compared": len(g_list), "matched": int(same.sum()),
                        "firings_compared": int(fir.sum()), "divergent": [int(g_list[i]) for i in np.nonzero(~same)[0]]}, f)
     assert same.all(), ("divergent trajectories", [g_list[i] for i in np.nonzero(~same)[0]][:10])
+
+
+def _overflow_models():
+    big = 2**31 - 7
+    # non-structural: influx at the top level pushes a count past int32
+    influx = {"name": "overflow-influx", "n_atoms": 2, "n_labels": 2,
+              "term": {"atoms": {0: big}, "comps": [{"label": 1, "wrap": {}, "content": {"atoms": {1: 3}}}]},
+              "rules": [{"label": 0, "atoms": {}, "rate": 1.0, "rhs": {"X": True, "atoms": {0: 2}}},
+                        {"label": 1, "atoms": {1: 1}, "rate": 0.5, "rhs": {"X": True, "atoms": {}}}],
+              "observables": [("content", 0, 0), ("content", 1, 1), ("count", 1)]}
+    # structural: lysis releases a cell's content into a top level that is near the limit
+    lysis = {"name": "overflow-lysis", "n_atoms": 1, "n_labels": 2,
+             "term": {"atoms": {0: big}, "comps": [{"label": 1, "wrap": {}, "content": {"atoms": {0: 5}}},
+                                                   {"label": 1, "wrap": {}, "content": {"atoms": {0: 9}}}]},
+             "rules": [{"label": 0, "atoms": {}, "rate": 0.7, "comp": {"label": 1, "wrap": {}, "content": {}},
+                        "rhs": {"X": True, "atoms": {}, "release_W": True, "release_Y": True}},
+                       {"label": 1, "atoms": {0: 1}, "rate": 0.3, "rhs": {"X": True, "atoms": {}}}],
+             "observables": [("content", 0, 0), ("content", 1, 0), ("count", 1)]}
+    return [influx, lysis]
+
+
+@pytest.mark.parametrize("which", [0, 1], ids=["influx", "lysis"])
+def test_overflow_status_matches_oracle(which):
+    model = _overflow_models()[which]
+    m = cwc_dyn.cwc_dyn_model_create(model)
+    n, t_end, dt = 40, 8.0, 0.25
+    gpu = cwc_dyn.simulate(m, n, t_end, dt, 2, want_traj=True)
+    torch.cuda.synchronize()
+    ora = dyn.simulate(model, 0, t_end, dt, 2, g_list=list(range(n)))
+    assert (gpu["status"].cpu().numpy() == ora["status"]).all()
+    assert (ora["status"] == 2).any()          # the case exercises OVERFLOW
+    assert (gpu["traj"].cpu().numpy() == ora["traj"]).all()
+    assert (gpu["firings"].cpu().numpy() == ora["firings"]).all()
