@@ -284,9 +284,12 @@ cwc_status cwc_simulate_host_workspace_size(cwc_model model, int64_t n_replicas,
 
 /*
  * mean = sum / count; var = (count * sumsq - sum^2) / (count (count - 1))
- * formed exactly in 128/256-bit integers and rounded once per division
- * (0 when count == 1); ci90 = 1.6449 * sqrt(var / count) (S:400-403,
- * S:418-427).  Device -> device over n_cells, on cuda_stream.
+ * (0 when count == 1): numerator (192-bit) and denominator (126-bit) are
+ * exact integers and each quotient is rounded to nearest-even ONCE (exact
+ * long division with a sticky bit), so mean and var are the correctly
+ * rounded values of the exact rationals; ci90 = 1.6449 * sqrt(var / count)
+ * in IEEE fp64 operations.  NaN where
+ * count == 0.  Device -> device over n_cells, on cuda_stream.
  */
 cwc_status cwc_stats_finalize(const cwc_stats *stats, int64_t n_cells, double *mean, double *var,
                               double *ci90, void *cuda_stream);

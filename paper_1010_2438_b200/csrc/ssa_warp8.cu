@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(128) ssa_group_kernel(const RunParams rp, cons
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gq = lane / LG, gl = lane & (LG - 1), gb = gq * LG;  // group, lane in group, group's first lane
-    const int M = wt.M, B4 = (M + LG - 1) / LG, NS = (B4 + 15) >> 4;
+    const int M = wt.M, B4 = (M + LG - 1) / LG;
+    const int NS = B4 > 0 ? (B4 + 15) >> 4 : 1;  // (a model without rules keeps one zeroed sub-chunk: the selection's reads stay in range)
     const int O = wt.O;
     const long long J = rp.J, J1 = J + 1;
     unsigned char *base = smem + (size_t)wib * per_warp_bytes;
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(128) ssa_group_kernel(const RunParams rp, cons
 }
 
 size_t group_smem_per_warp(const WarpTables &wt, int LG) {  // aw [16 NS][32], ss [4][32], dr [32][TPW], x [cells + 1][TPW]
-    const int B = (wt.M + LG - 1) / LG, NS = (B + 15) >> 4, TPW = 32 / LG;
+    const int B = (wt.M + LG - 1) / LG, NS = B > 0 ? (B + 15) >> 4 : 1, TPW = 32 / LG;
     return (size_t)8 * 16 * NS * 32 + (size_t)8 * 4 * 32 + (size_t)16 * 32 * TPW + (size_t)4 * TPW * (wt.n_cells + 1);
 }
 

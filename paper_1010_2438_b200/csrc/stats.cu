@@ -101,10 +101,44 @@ __device__ __forceinline__ U192 sub_192_128(U192 a, unsigned __int128 b) {
     return r;
 }
 
-__device__ __forceinline__ double u192_to_double(U192 a) {
-    // exact scaling by powers of two; the sum rounds once per term
-    return __dadd_rn(__dadd_rn(__dmul_rn(__ull2double_rn(a.w[2]), 0x1.0p128), __dmul_rn(__ull2double_rn(a.w[1]), 0x1.0p64)),
-                     __ull2double_rn(a.w[0]));
+// RN(N / D) for 0 <= N < 2^192, 0 < D < 2^126: the quotient's binary expansion
+// by restoring division, one bit per step from N's most significant set bit
+// on.  The first 64 significant quotient bits are kept, every later bit and
+// the final remainder fold into a sticky bit below them (11 bits under the
+// rounding position), so the single conversion rounds the exact quotient to
+// nearest-even once; the power-of-two scaling is exact (|result| >= 2^-126).
+__device__ double div_rn_u192(U192 N, unsigned __int128 D) {
+    int top = -1;
+    for (int w = 2; w >= 0 && top < 0; --w)
+        if (N.w[w]) top = 64 * w + 63 - __clzll((long long)N.w[w]);
+    if (top < 0) return 0.0;
+    unsigned __int128 rem = 0;  // < D < 2^126, so (rem << 1) | bit fits
+    unsigned long long mant = 0;
+    int nbits = 0, e_first = 0;  // kept bits; weight exponent of the first significant quotient bit
+    bool sticky = false;
+    // quotient bits at weights 2^pos: every integer position (pos >= 0), then
+    // fractional ones while fewer than 64 bits are kept and the remainder is non-zero
+    for (int pos = top;; --pos) {
+        if (pos < 0 && (nbits >= 64 || rem == 0)) break;
+        const unsigned long long bit = (pos >= 0) ? ((N.w[pos >> 6] >> (pos & 63)) & 1ull) : 0ull;
+        rem = (rem << 1) | bit;
+        const bool q = rem >= D;
+        if (q) rem -= D;
+        if (nbits < 64) {
+            if (nbits > 0 || q) {
+                if (nbits == 0) e_first = pos;
+                mant = (mant << 1) | (q ? 1ull : 0ull);
+                ++nbits;
+            }
+        } else if (q) {
+            sticky = true;
+        }
+    }
+    if (rem != 0) sticky = true;
+    mant <<= (64 - nbits);  // N > 0, so 1 <= nbits <= 64
+    const int last = e_first - 63;  // weight exponent of mant's bit 0
+    if (sticky) mant |= 1ull;
+    return scalbn(__ull2double_rn(mant), last);
 }
 
 __global__ void stats_finalize_kernel(const int64_t *count, const int64_t *sum, const uint64_t *sumsq, long long n,
@@ -115,15 +149,17 @@ __global__ void stats_finalize_kernel(const int64_t *count, const int64_t *sum, 
         const unsigned __int128 s2 = (unsigned __int128)sumsq[2 * c] | ((unsigned __int128)sumsq[2 * c + 1] << 64);
         double m = __longlong_as_double(0x7ff8000000000000ll), v = m, ci = m;
         if (cnt > 0) {
-            m = __ddiv_rn(__ull2double_rn(s1), __ll2double_rn(cnt));
+            U192 s;
+            s.w[0] = s1;
+            s.w[1] = s.w[2] = 0;
+            m = div_rn_u192(s, (unsigned __int128)cnt);
             if (cnt == 1) {
                 v = 0.0;
                 ci = 0.0;
             } else {
                 const U192 num = sub_192_128(mul_64x128((unsigned long long)cnt, s2), (unsigned __int128)s1 * s1);
-                const double den = __dmul_rn(__ll2double_rn(cnt), __ll2double_rn(cnt - 1));
-                v = __ddiv_rn(u192_to_double(num), den);
-                ci = __dmul_rn(1.6449, sqrt(__ddiv_rn(v, __ll2double_rn(cnt))));
+                v = div_rn_u192(num, (unsigned __int128)cnt * (unsigned long long)(cnt - 1));
+                ci = __dmul_rn(1.6449, __dsqrt_rn(__ddiv_rn(v, __ll2double_rn(cnt))));
             }
         }
         if (mean) mean[c] = m;

@@ -207,6 +207,9 @@ def test_stats_modes_agree(mode):
 
 
 def test_finalize_matches_oracle_moments():
+    """Mean, variance and ci90 of a run equal the oracle's bit for bit: the
+    device forms every quotient exactly and rounds it once (cwc.h,
+    cwc_stats_finalize), like the oracle's Fraction -> float."""
     desc, _, _ = w.config("C1")
     cfg = dict(t_end=100.0, sample_dt=1.0, n_replicas=1024, seed=1)
     gpu = _gpu(cwc.cwc_model_create(desc), cfg, finalize=True)
@@ -214,8 +217,52 @@ def test_finalize_matches_oracle_moments():
     means, vars_, cis = oracle.finalize(o["count"], o["sum"], o["sumsq"])
     for got, want in ((gpu["mean"], means), (gpu["var"], vars_), (gpu["ci90"], cis)):
         g = got.cpu().numpy().reshape(-1)
-        wv = np.asarray(want)
-        assert np.all(np.abs(g - wv) <= 1e-9 * np.maximum(np.abs(g), np.abs(wv)))
+        wv = np.asarray(want, dtype=np.float64)
+        assert np.array_equal(g.view(np.uint64), wv.view(np.uint64))
+
+
+def test_finalize_exact_rounding_on_wide_moments():
+    """cwc_stats_finalize on synthetic moment cells spanning the whole
+    accumulator range (counts to 2^40, sums to 2^63, 128-bit sums of
+    squares; numerators and denominators far beyond 2^53, tiny and huge
+    quotients, exact and halfway cases): mean and variance equal the
+    oracle's correctly rounded Fraction quotients bit for bit."""
+    rng = np.random.default_rng(7)
+    cells = []  # (n, s1, s2) Python ints with n*s2 >= s1^2
+    # values v_i in a block: n copies split between a and b  ->  exact moments
+    for _ in range(300):
+        n = int(rng.integers(2, 1 << int(rng.integers(2, 41))))
+        a = int(rng.integers(0, 1 << int(rng.integers(1, 24))))
+        b = a + int(rng.integers(0, 1 << int(rng.integers(1, 23))))
+        k = int(rng.integers(0, n + 1))  # k values equal a, n - k equal b
+        s1 = k * a + (n - k) * b
+        s2 = k * a * a + (n - k) * b * b
+        if s1 < (1 << 63):
+            cells.append((n, s1, s2))
+    # hand-made: zero variance, count 1, count 0, halfway quotients, huge s2
+    cells += [(5, 35, 245), (1, 7, 49), (0, 0, 0), (2, 1, 1), (3, 1, 1), (2, (1 << 53) + 1, ((1 << 53) + 1) ** 2),
+              (1 << 40, (1 << 62) + 12345, ((1 << 84) + 999) + (1 << 100)), (3, 2**53 + 1, (2**53 + 1) ** 2),
+              (7, 6, 36), (1 << 20, 3, 9), ((1 << 40) - 1, (1 << 40) - 1, (1 << 40) - 1)]
+    cells = [c for c in cells if c[0] * c[2] >= c[1] * c[1]]
+    n = len(cells)
+    cnt = torch.tensor([c[0] for c in cells], dtype=torch.int64, device="cuda")
+    s1 = torch.tensor([c[1] for c in cells], dtype=torch.int64, device="cuda")
+    lo = np.array([c[2] & ((1 << 64) - 1) for c in cells], dtype=np.uint64)
+    hi = np.array([c[2] >> 64 for c in cells], dtype=np.uint64)
+    sq = torch.from_numpy(np.stack([lo, hi], axis=1).view(np.int64).copy()).cuda()
+    mean = torch.empty(n, dtype=torch.float64, device="cuda")
+    var = torch.empty_like(mean)
+    ci = torch.empty_like(mean)
+    cwc.cwc_stats_finalize((cnt, s1, sq), n, mean, var, ci, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    gm, gv, gc = mean.cpu().numpy(), var.cpu().numpy(), ci.cpu().numpy()
+    for i, (c, a, b) in enumerate(cells):
+        m, v, z = oracle.moments.finalize_cell(c, a, b)
+        for got, want in ((gm[i], m), (gv[i], v), (gc[i], z)):
+            if math.isnan(want):
+                assert math.isnan(got), (cells[i], got)
+            else:
+                assert np.float64(got).view(np.uint64) == np.float64(want).view(np.uint64), (cells[i], got, want)
 
 
 @pytest.mark.parametrize("kern", [cwc.CWC_KERNEL_WARP2, cwc.CWC_KERNEL_WARP, cwc.CWC_KERNEL_WARP8,
