@@ -279,3 +279,23 @@ def test_plan_picks_the_warp_kernel_by_network_size():
     assert kern(w.config("C4")[0], kernel=cwc.CWC_KERNEL_WARP8) == cwc.CWC_KERNEL_WARP8
     with pytest.raises(cwc.CwcError):
         kern(w.config("C5")[0], kernel=cwc.CWC_KERNEL_WARP8)
+
+
+def test_plan_of_a_model_without_rules_keeps_the_selection_rows():
+    """A model with no rules (M = 0) still plans on every warp kernel, and the
+    group kernels reserve one (zeroed) 16-row sub-chunk of propensities per
+    warp: their selection reads rows [0, 16) of the chosen sub-chunk even for
+    a trajectory that stalls at once (ssa_warp8.cu, NS >= 1)."""
+    desc = w.decay_model(5, 1.0)
+    desc["rules"] = []
+    m = cwc.cwc_model_create(desc)
+    assert m.info.n_reactions == 0
+    for kern, lg in ((cwc.CWC_KERNEL_WARP8, 4), (cwc.CWC_KERNEL_WARP4, 8)):
+        p = cwc.cwc_plan(m, 33, None, 2.0, 0.5, _opts(kernel=kern))
+        assert p.kernel == kern
+        warps = p.threads // 32
+        rows = 8 * 16 * 32  # one sub-chunk of fp64 rows [16][32]
+        per_warp = rows + 8 * 4 * 32 + 16 * 32 * (32 // lg) + 4 * (32 // lg) * (m.info.n_cells + 1)
+        assert p.smem_bytes >= warps * per_warp, (kern, p.smem_bytes, warps, per_warp)
+    for kern in (cwc.CWC_KERNEL_WARP, cwc.CWC_KERNEL_WARP2):
+        assert cwc.cwc_plan(m, 33, None, 2.0, 0.5, _opts(kernel=kern)).kernel == kern
