@@ -7,7 +7,10 @@ import torch
 
 sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
 import workloads.dynamic as wd  # noqa: E402
-from paper_1010_2438_b200 import cwc_dyn  # noqa: E402
+from paper_1010_2438_b200 import cwc, cwc_dyn  # noqa: E402
+
+if __import__("os").environ.get("CWC_PROBE_LIB"):  # an experiment variant (tools/build_variant.sh)
+    cwc.LIB_PATH = __import__("os").path.abspath(__import__("os").environ["CWC_PROBE_LIB"])
 
 
 def main():

@@ -13,6 +13,10 @@ import workloads as wl  # noqa: E402
 from bench import ClockSampler  # noqa: E402
 from paper_1010_2438_b200 import cwc  # noqa: E402
 
+if len(sys.argv) > 1:  # an experiment variant of the library (tools/build_variant.sh)
+    cwc.LIB_PATH = os.path.abspath(sys.argv[1])
+LIBTAG = os.path.basename(cwc.LIB_PATH)
+
 cases = [("rnd", M, lambda M=M: wl.random_network_model(seed=1, n_species=64, n_reactions=M)) for M in (64, 96, 128, 160, 192, 224, 256)]
 cases += [("lv", 129, lambda: wl.lotka_volterra_chain(128))]
 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -34,5 +38,5 @@ for name, M, make in cases:
             best = ms if best is None else min(best, ms)
         c = clk.stop()
         f = float(out["firings"].double().sum())
-        print(json.dumps({"model": name, "M": model.info.n_reactions, "cells": model.info.n_cells, "kernel": kname,
+        print(json.dumps({"lib": LIBTAG, "model": name, "M": model.info.n_reactions, "cells": model.info.n_cells, "kernel": kname,
                           "firings": f, "ms": best, "firings_per_s": f / best * 1e3, "clocks": c}), flush=True)
