@@ -74,9 +74,17 @@ template <int BMAX>
 __device__ __forceinline__ double chunk_sum(const double *ch, int B) {
     double s = ch[0];
     if constexpr (BMAX > 0) {
+        if (B > BMAX - 4) {  // nearly full chunk: no per-entry bounds tests below BMAX - 4 (warp-uniform)
 #pragma unroll
-        for (int k = 1; k < BMAX; ++k)
-            if (k < B) s = __dadd_rn(s, ch[k]);
+            for (int k = 1; k < BMAX - 4; ++k) s = __dadd_rn(s, ch[k]);
+#pragma unroll
+            for (int k = BMAX - 4; k < BMAX; ++k)
+                if (k < B) s = __dadd_rn(s, ch[k]);
+        } else {
+#pragma unroll
+            for (int k = 1; k < BMAX; ++k)
+                if (k < B) s = __dadd_rn(s, ch[k]);
+        }
     } else {
 #pragma unroll 4
         for (int k = 1; k < B; ++k) s = __dadd_rn(s, ch[k]);
@@ -94,9 +102,17 @@ __device__ __forceinline__ double chunk_sum4(const double *ch, int B) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) s[r] = (r < B) ? ch[r] : 0.0;
     if constexpr (BMAX > 0) {
+        if (B > BMAX - 4) {  // nearly full chunk (C5: 37 of 40): bounds tests on the last four entries only
 #pragma unroll
-        for (int k = 4; k < BMAX; ++k)
-            if (k < B) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+            for (int k = 4; k < BMAX - 4; ++k) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+#pragma unroll
+            for (int k = BMAX - 4; k < BMAX; ++k)
+                if (k < B) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+        } else {
+#pragma unroll
+            for (int k = 4; k < BMAX; ++k)
+                if (k < B) s[k & 3] = __dadd_rn(s[k & 3], ch[k]);
+        }
     } else {
         int k = 4;
         for (; k + 3 < B; k += 4) {
