@@ -211,6 +211,7 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
         __syncwarp();
 
         double part = 0.0;
+        constexpr bool AHEAD = MINB <= 6;  // register budget for values loaded or computed ahead of their use (below)
         constexpr bool SUM4 = (BMAX == 0 || BMAX > 16);  // long chunks: chunk_sum4, also here
         for (int k = 0; k < B; ++k) {
             const int m = lane * B + k;
@@ -254,8 +255,25 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             const int i = kd;
             const double E = shfl_d(El, i);
             const double u2 = shfl_d(u2l, i);
-            // warp-uniform operands: the fast/IEEE choice never diverges
-            const double tau = div_fast_ok(E, a0) ? div_fast(E, a0) : __ddiv_rn(E, a0);
+            // warp-uniform operands: the fast/IEEE choice never diverges.
+            // AHEAD (the 80-register instantiations): the fast quotient is
+            // formed unconditionally, ahead of the test that says whether it
+            // is the IEEE one, together with the first stage of the selection
+            // (which needs a0 and u2 only): the division's dependent fp64
+            // chain then overlaps the ballot and shuffle latencies instead of
+            // standing alone on the firing's critical path (C5 +5 % with the
+            // dependency prefetch below; the 64-register instantiations lose
+            // 5 % to the extra live values and keep the plain order)
+            double qf = 0.0, target = 0.0, carry = 0.0;
+            int L = 0;
+            if constexpr (AHEAD) {
+                qf = div_fast(E, a0);
+                target = __dmul_rn(u2, a0);
+                const unsigned hitsL = __ballot_sync(kFull, incl > target);
+                L = hitsL ? __ffs(hitsL) - 1 : 0;  // lane 31's prefix is a0 > target (a0 == 0: stall below)
+                carry = shfl_d(excl, L);
+            }
+            const double tau = div_fast_ok(E, a0) ? (AHEAD ? qf : div_fast(E, a0)) : __ddiv_rn(E, a0);
             const double tn = __dadd_rn(t, tau);
             if (!(tn < t_next)) {
                 if (a0 == 0.0) {
@@ -274,10 +292,12 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
                 }
                 t_next = __dmul_rn(__int2double_rn(j), rp.dt);
             }
-            const double target = __dmul_rn(u2, a0);
-            const int L = __ffs(__ballot_sync(kFull, incl > target)) - 1;  // lane 31's prefix is a0 > target
+            if constexpr (!AHEAD) {
+                target = __dmul_rn(u2, a0);
+                L = __ffs(__ballot_sync(kFull, incl > target)) - 1;  // lane 31's prefix is a0 > target
+                carry = shfl_d(excl, L);
+            }
             // inside chunk L: shuffle-scan its entries from L's exclusive prefix
-            double carry = shfl_d(excl, L);
             int mu = -1;
             unsigned pos_any = 0;
             int pos_base = 0;
@@ -327,6 +347,12 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             // The per-mu header (nu offset, nu count, dependency offset,
             // dependency count) is one load.
             const int4 h = __ldg(wt.hdr + mu);
+            // the first round of dependency entries is requested now: the L2
+            // round trip of the D(mu) list (the longest load on the firing's
+            // chain) overlaps the count update below (read-only table; nothing
+            // uses the entry before the update is done)
+            int4 dq = make_int4(0, 0, 0, 0);
+            if (AHEAD && lane < h.w) dq = __ldcg(wt.depw32 + (h.z + lane));  // L2 only: the D(mu) lists stream (C5: 330 KB) and would evict the per-mu header, net-change and rate tables from L1
             int2 e = make_int2(0, 0);
             long long nv = 0;
             if (lane < h.y) {
@@ -345,11 +371,13 @@ __global__ void __launch_bounds__(128, MINB) ssa_warp_kernel(const RunParams rp,
             // (byte-offset entries and A + A-halved rates: see ssa_warp2.cu).
             unsigned dirty = 0;
 #pragma unroll 1
-            for (int q = lane; q < h.w; q += 32) {
-                const int4 d = __ldcg(wt.depw32 + h.z + q);  // L2 only: the D(mu) lists stream (C5: 330 KB) and would evict the per-mu header, net-change and rate tables from L1
+            for (int q = lane; q < h.w;) {
+                const int4 d = AHEAD ? dq : __ldcg(wt.depw32 + (h.z + q));
+                q += 32;
+                if (AHEAD && q < h.w) dq = __ldcg(wt.depw32 + (h.z + q));  // (more than 32 dependents: the next round, in flight during this one)
+                const double k = __ldg((const double *)((const unsigned char *)rates_h + (d.w & 0x3ffffff)));
                 const int xa = *(const int *)((const unsigned char *)xs + d.y);
                 const int xb = *(const int *)((const unsigned char *)xs + d.z) - (int)((unsigned)d.w >> 31);
-                const double k = __ldg((const double *)((const unsigned char *)rates_h + (d.w & 0x3ffffff)));
                 *(double *)((unsigned char *)as + d.x) = __dmul_rn(k, __dmul_rn(__int2double_rn(xa), __int2double_rn(xb)));
                 dirty |= 1u << (((unsigned)d.w >> 26) & 31u);
             }
