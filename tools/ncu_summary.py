@@ -60,6 +60,31 @@ def summarise(rep):
                 pass
     st.sort(key=lambda x: -x[1])
     s["stalls_per_issue"] = dict(st[:8])
+    # pipe mix: warp instructions per pipe, as fractions of all executed
+    pipes = {}
+    for h, (v, u) in d.items():
+        if h.startswith("sm__inst_executed_pipe_") and h.endswith(".sum"):
+            try:
+                pipes[h[len("sm__inst_executed_pipe_"):-len(".sum")]] = float(v.replace(",", ""))
+            except ValueError:
+                pass
+    if pipes and s.get("warp_inst"):
+        s["pipe_mix"] = {k: round(v / s["warp_inst"], 4) for k, v in sorted(pipes.items(), key=lambda x: -x[1]) if v > 0}
+    # derived: issue fraction per elapsed cycle, SIMT efficiency, useful issue, divergent branch targets
+    for k, name in (("inst_issued", "smsp__inst_issued.sum"), ("smsp_cycles_elapsed", "smsp__cycles_elapsed.sum")):
+        if name in d:
+            try:
+                s[k] = float(d[name][0].replace(",", ""))
+            except ValueError:
+                pass
+    if s.get("inst_issued") and s.get("smsp_cycles_elapsed"):
+        s["issue_fraction_elapsed"] = s["inst_issued"] / s["smsp_cycles_elapsed"]
+    if isinstance(s.get("threads_per_inst"), float):
+        s["simt_efficiency"] = s["threads_per_inst"] / 32.0
+        if "issue_fraction_elapsed" in s:
+            s["useful_issue"] = s["issue_fraction_elapsed"] * s["simt_efficiency"]
+    if s.get("branch_targets") and "branch_targets_divergent" in s:
+        s["divergent_branch_target_ratio"] = s["branch_targets_divergent"] / s["branch_targets"]
     if "dram_read_bytes" in s and "dram_write_bytes" in s:
         s["dram_bytes"] = s["dram_read_bytes"] + s["dram_write_bytes"]
     return s
