@@ -21,6 +21,7 @@ __global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n
     const int lb = stat_limb_bits(L);
     const long long pb = stat_bytes(L, rp.cells_per_part);
     const long long n = rp.cells_per_part;
+    const bool sq16 = (reinterpret_cast<unsigned long long>(sumsq) & 15ull) == 0ull;
     for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n_cells;
          c += (long long)gridDim.x * blockDim.x) {
         const long long p = c / JO;
@@ -34,30 +35,35 @@ __global__ void stats_stage2_kernel(const RunParams rp, long long O, long long n
             b0 = 0;
             b1 = rp.n_parts - 1;
         }
-        // per-word totals over the parts (each word < 2^64 per part; at most
-        // 2^31 parts) accumulated in 128 bits, then limbs recombined
-        unsigned __int128 w[1 + 8 + 16];
-        const int nw = stat_words(L);
-        for (int k = 0; k < nw; ++k) w[k] = 0;
+        // the parts' limb words summed straight into the recombined 128-bit
+        // totals: sum_b sum_i (u[b][i] << lb i) (arithmetic mod 2^128, so the
+        // order of the two sums does not matter; the true totals fit by the
+        // planner's bound).  No per-thread word array (it lived in local memory).
+        unsigned __int128 cnt = 0, s1 = 0, s2 = 0;
         for (long long b = b0; b <= b1; ++b) {
             long long local = c;
             if (rp.traj_per_part > 0) local = (p - (b * rp.traj_per_part) / rp.R) * JO + rest;
             const unsigned char *base = (const unsigned char *)rp.parts + b * pb;
             if (L.wb == 4) {
                 const unsigned int *u = (const unsigned int *)base + local;
-                for (int k = 0; k < nw; ++k) w[k] += u[(long long)k * n];
+                cnt += u[0];
+                for (int i = 0; i < L.sl; ++i) s1 += (unsigned __int128)u[(long long)(1 + i) * n] << (lb * i);
+                for (int i = 0; i < L.ql; ++i) s2 += (unsigned __int128)u[(long long)(1 + L.sl + i) * n] << (lb * i);
             } else {
                 const unsigned long long *u = (const unsigned long long *)base + local;
-                for (int k = 0; k < nw; ++k) w[k] += u[(long long)k * n];
+                cnt += u[0];
+                for (int i = 0; i < L.sl; ++i) s1 += (unsigned __int128)u[(long long)(1 + i) * n] << (lb * i);
+                for (int i = 0; i < L.ql; ++i) s2 += (unsigned __int128)u[(long long)(1 + L.sl + i) * n] << (lb * i);
             }
         }
-        unsigned __int128 s1 = 0, s2 = 0;
-        for (int i = 0; i < L.sl; ++i) s1 += w[1 + i] << (lb * i);
-        for (int i = 0; i < L.ql; ++i) s2 += w[1 + L.sl + i] << (lb * i);
-        count[c] = (int64_t)w[0];
+        count[c] = (int64_t)cnt;
         sum[c] = (int64_t)s1;
-        sumsq[2 * c] = (uint64_t)s2;
-        sumsq[2 * c + 1] = (uint64_t)(s2 >> 64);
+        if (sq16) {  // one 16-byte store per cell (coalesced, vectorised) when the array is 16-byte aligned
+            reinterpret_cast<ulonglong2 *>(sumsq)[c] = make_ulonglong2((unsigned long long)s2, (unsigned long long)(s2 >> 64));
+        } else {
+            sumsq[2 * c] = (uint64_t)s2;
+            sumsq[2 * c + 1] = (uint64_t)(s2 >> 64);
+        }
     }
 }
 
