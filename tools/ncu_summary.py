@@ -63,9 +63,9 @@ def summarise(rep):
     # pipe mix: warp instructions per pipe, as fractions of all executed
     pipes = {}
     for h, (v, u) in d.items():
-        if h.startswith("sm__inst_executed_pipe_") and h.endswith(".sum"):
+        if "inst_executed_pipe_" in h and h.endswith(".sum"):  # sm__ or smsp__ prefixed, per the ncu version
             try:
-                pipes[h[len("sm__inst_executed_pipe_"):-len(".sum")]] = float(v.replace(",", ""))
+                pipes[h[h.index("inst_executed_pipe_") + len("inst_executed_pipe_"):-len(".sum")]] = float(v.replace(",", ""))
             except ValueError:
                 pass
     if pipes and s.get("warp_inst"):
