@@ -68,6 +68,18 @@ def summarise(rep):
                 pipes[h[h.index("inst_executed_pipe_") + len("inst_executed_pipe_"):-len(".sum")]] = float(v.replace(",", ""))
             except ValueError:
                 pass
+    # per-pipe utilisation (what `--set full` carries): instructions executed on the pipe, % of that pipe's peak
+    util = {}
+    for h, (v, u) in d.items():
+        if h.startswith("sm__inst_executed_pipe_") and h.endswith(".avg.pct_of_peak_sustained_active"):
+            try:
+                x = float(v.replace(",", ""))
+            except ValueError:
+                continue
+            if x >= 0.5:
+                util[h[len("sm__inst_executed_pipe_"):-len(".avg.pct_of_peak_sustained_active")]] = round(x, 2)
+    if util:
+        s["pipe_util_pct"] = dict(sorted(util.items(), key=lambda x: -x[1]))
     if pipes and s.get("warp_inst"):
         s["pipe_mix"] = {k: round(v / s["warp_inst"], 4) for k, v in sorted(pipes.items(), key=lambda x: -x[1]) if v > 0}
     # derived: issue fraction per elapsed cycle, SIMT efficiency, useful issue, divergent branch targets
